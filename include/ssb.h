@@ -1,0 +1,129 @@
+/*
+ * ssb.h -- C ABI of the B200 deskew + projection library (libssb.so).
+ *
+ * The reference (skewstream, pure Python/numpy) has no FFI layer: its boundary
+ * is the Python API.  Each entry point below replaces one reference function on
+ * the hot path; the Python drop-in (paper_2211_00645_b200/) binds them with
+ * ctypes.  No torch types cross this boundary: device buffers are plain
+ * pointers (the caller owns them; the library never keeps a pointer past the
+ * call), sizes are int64, the stream is an opaque cudaStream_t (NULL = legacy
+ * default stream).  Every call is asynchronous on that stream.
+ *
+ * Data layout (reference file:line):
+ *   raw frames  (n, H, W) uint16 C-order, W contiguous            ss/pipeline.py:34-61
+ *   volume      (n, U, W) uint16 C-order, zero outside each slice ss/phantom.py:390 (the "pile")
+ *   XY          (U, W)  = reduce over slices (axis 0)             ss/pipeline.py:316-336
+ *   XZ          (n, W)  = reduce over canvas rows (axis 1)        north_star extension
+ *   YZ          (n, U)  = reduce over columns (axis 2)            north_star extension
+ *   max -> uint16, sum -> uint32 (sum of the rounded uint16 voxels, exact)
+ * U = H + ceil((N-1)*s - 1e-9) (ss/geometry.py:129-147); a call may cover a
+ * window of canvas rows [u_begin, u_begin + u_count) (scan-axis slabs).
+ */
+#ifndef SSB_H
+#define SSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSB_VERSION 100
+
+/* status codes; Python maps them onto ss/errors.py classes */
+#define SSB_OK 0
+#define SSB_ERR_PARAM 1    /* ParameterError (a ValueError)   ss/errors.py:8  */
+#define SSB_ERR_CAPACITY 2 /* CapacityError                   ss/errors.py:12 */
+#define SSB_ERR_PROTOCOL 3 /* ProtocolError                   ss/errors.py:16 */
+#define SSB_ERR_CUDA 4     /* SkewstreamError (device failure)                */
+
+#define SSB_INTERP_NEAREST 0 /* ss/geometry.py:236-243 placement, frame rows copied  */
+#define SSB_INTERP_LINEAR 1  /* ss/geometry.py:246-255 span, two-row lerp per frame  */
+
+#define SSB_FORMULA_CANVAS 0   /* ss/pipeline.py:229-236  rint((1-f)*a + f*b), fp64 */
+#define SSB_FORMULA_NPINTERP 1 /* ss/phantom.py:396-402   np.interp per column, fp64 */
+
+#define SSB_REDUCE_MAX 0
+#define SSB_REDUCE_SUM 1
+
+/* flags */
+#define SSB_FLAG_XY_ACCUMULATE 1 /* xy = reduce(xy, new) instead of xy = new (canvas place) */
+
+typedef struct ssb_deskew_desc {
+    int64_t n;           /* frames in this call                                    */
+    int64_t height;      /* H, rows per frame (oblique / sheet-depth axis)         */
+    int64_t width;       /* W, columns per frame (invariant axis, contiguous)      */
+    int64_t first_slice; /* global scan index of frame 0 (slabs keep global i*s)   */
+    double shear_px;     /* s, canvas rows per slice (>= 0)                        */
+    int32_t interp;      /* SSB_INTERP_*                                           */
+    int32_t formula;     /* SSB_FORMULA_*                                          */
+    int64_t u_begin;     /* first canvas row covered                               */
+    int64_t u_count;     /* canvas rows covered (volume / XY / YZ row extent)      */
+    int32_t reduce;      /* SSB_REDUCE_*                                           */
+    int32_t flags;       /* SSB_FLAG_*                                             */
+} ssb_deskew_desc;
+
+/* Library version (SSB_VERSION) and the last error message of this thread. */
+int ssb_version(void);
+const char *ssb_last_error(void);
+
+/* Number of kernels this library has launched in the process (for the bench). */
+int64_t ssb_launch_count(void);
+
+/*
+ * Kernel timing for the benchmark (per calling thread): while enabled, every
+ * ssb_deskew records a CUDA event pair around its main fused kernel on the
+ * launch stream.  ssb_profile_read waits for the recorded events, returns the
+ * summed device milliseconds and the number of timed launches, and clears them.
+ */
+int ssb_profile_enable(int32_t on);
+int ssb_profile_read(double *total_ms, int64_t *launches);
+
+/* Scratch bytes ssb_deskew needs for partial projections. */
+size_t ssb_deskew_workspace_bytes(const ssb_deskew_desc *d);
+
+/*
+ * Fused deskew + projections.  Replaces, for a whole stack or a slab of it:
+ *   ProjectionCanvas.place x n + finalize_global   ss/pipeline.py:316-336  (formula CANVAS)
+ *   phantom.reference_deskew                       ss/phantom.py:359-402   (formula NPINTERP)
+ *   _interp_slice_rows per slice                   ss/pipeline.py:229-236
+ * raw: device (n, H, W) uint16.  vol: device (n, u_count, W) uint16 or NULL.
+ * xy (u_count, W), xz (n, W), yz (n, u_count): device, uint16 (max) or
+ * uint32 (sum), each may be NULL.  workspace: device, >= ssb_deskew_workspace_bytes.
+ * Pointers must be 16-byte aligned for the vectorised path (any alignment works).
+ */
+int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz,
+               void *yz, void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Rolling-mode band recompute.  Replaces ProjectionCanvas._recompute_band
+ * (ss/pipeline.py:361-377): canvas rows [lo, hi] become the strict-'>' max over
+ * the live ring slices (present[k] != 0) with contributor = first maximal ring
+ * index, -1 where nothing contributes.  ring: device (n_ring, H, W) uint16 where
+ * ring slot k holds global slice k; canvas (U, W) uint16, contributor (U, W) int16.
+ */
+int ssb_rolling_band(const uint16_t *ring, const uint8_t *present, int64_t n_ring, int64_t height,
+                     int64_t width, double shear_px, int32_t interp, int64_t lo, int64_t hi,
+                     uint16_t *canvas, int16_t *contributor, int64_t canvas_rows, void *stream);
+
+/*
+ * Display warp.  Replaces warp_projection (ss/pipeline.py:434-457): out row m
+ * samples input row clip(m / scale, 0, rows-1) with an fp64 lerp and rint;
+ * scale == 1.0 is a copy.  out_rows = round(rows * scale) (caller computes).
+ */
+int ssb_warp_rows(const uint16_t *proj, int64_t rows, int64_t cols, double warp_scale,
+                  uint16_t *out, int64_t out_rows, void *stream);
+
+/*
+ * Projection combine for multi-GPU gathers: dst[k] = reduce(dst[k], src[k]) for
+ * count elements of uint16 (elem_bits 16, max) or uint32 (elem_bits 32, max/sum).
+ */
+int ssb_combine(const void *src, void *dst, int64_t count, int32_t reduce, int32_t elem_bits,
+                void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSB_H */

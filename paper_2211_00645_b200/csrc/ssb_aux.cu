@@ -1,0 +1,235 @@
+// Rolling-mode band recompute, display warp, projection combine, and the small
+// library entry points (version, last error, launch counter).
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ssb_common.cuh"
+#include "ssb_host.h"
+
+namespace ssb {
+
+namespace {
+thread_local std::string g_error;
+std::atomic<int64_t> g_launches{0};
+}  // namespace
+
+void set_error(const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_error = buf;
+}
+
+void count_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+namespace {
+struct Profiler {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t take() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+thread_local Profiler g_prof;
+}  // namespace
+
+void profile_begin(cudaStream_t st) {
+    if (!g_prof.on) return;
+    cudaEvent_t a = g_prof.take(), b = g_prof.take();
+    cudaEventRecord(a, st);
+    g_prof.pending.emplace_back(a, b);
+}
+
+void profile_end(cudaStream_t st) {
+    if (!g_prof.on || g_prof.pending.empty()) return;
+    cudaEventRecord(g_prof.pending.back().second, st);
+}
+
+namespace {
+
+// ss/pipeline.py:361-377.  One thread per (row, column) of the band.  Ring slot
+// k holds global slice k; the value it offers row u is the same sampled value
+// place() would use (canvas formula); strict '>' keeps the first maximum in
+// ring order; contributor -1 where every offer is 0 / absent.
+template <int INTERP>
+__global__ void rolling_band_kernel(const uint16_t *__restrict__ ring, const uint8_t *__restrict__ present,
+                                    int64_t n_ring, int64_t h, int64_t w, double s, int64_t lo,
+                                    int64_t hi, uint16_t *__restrict__ canvas,
+                                    int16_t *__restrict__ contrib) {
+    const int64_t total = (hi - lo + 1) * w;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = lo + e / w;
+        const int64_t x = e % w;
+        // slices whose span can contain u: i*s within [u-H-1, u+1] (exact check below)
+        int64_t k_lo = 0, k_hi = n_ring - 1;
+        if (s > 0.0) {
+            const double kl = floor(((double)(u - h) - 2.0) / s);
+            const double kh = ceil(((double)u + 2.0) / s);
+            k_lo = kl <= 0.0 ? 0 : (kl >= (double)n_ring ? n_ring : (int64_t)kl);
+            k_hi = kh >= (double)(n_ring - 1) ? n_ring - 1 : (kh < 0.0 ? -1 : (int64_t)kh);
+        }
+        uint32_t best = 0;
+        int32_t who = -1;
+        for (int64_t k = k_lo; k <= k_hi; ++k) {
+            if (!present[k]) continue;
+            int64_t klo, khi;
+            double off;
+            slice_span(k, s, h, INTERP, klo, khi, off);
+            if (u < klo || u > khi) continue;
+            const RowParam rp = row_param<INTERP, SSB_FORMULA_CANVAS>(u, klo, off, h);
+            const uint16_t *frame = ring + (size_t)k * h * w;
+            const uint32_t a = frame[(size_t)rp.j0 * w + x];
+            uint32_t v = a;
+            if (rp.kind == 2) v = lerp_voxel<SSB_FORMULA_CANVAS>(a, frame[(size_t)rp.j1 * w + x], rp);
+            if (v > best) {
+                best = v;
+                who = (int32_t)k;
+            }
+        }
+        canvas[u * w + x] = (uint16_t)best;
+        contrib[u * w + x] = (int16_t)who;
+    }
+}
+
+// ss/pipeline.py:451-457: m = clip(arange/scale, 0, rows-1); lerp rows m0, m1; rint.
+__global__ void warp_rows_kernel(const uint16_t *__restrict__ proj, int64_t rows, int64_t cols,
+                                 double scale, uint16_t *__restrict__ out, int64_t out_rows) {
+    const int64_t total = out_rows * cols;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = e / cols, c = e % cols;
+        double mm = __ddiv_rn((double)m, scale);
+        mm = fmin(fmax(mm, 0.0), (double)(rows - 1));
+        const int64_t m0 = (int64_t)floor(mm);
+        const int64_t m1 = m0 + 1 < rows - 1 ? m0 + 1 : rows - 1;
+        RowParam rp;
+        rp.c1 = __dsub_rn(mm, (double)m0);
+        rp.c0 = __dsub_rn(1.0, rp.c1);
+        rp.kind = 2;
+        out[e] = (uint16_t)lerp_voxel<SSB_FORMULA_CANVAS>(proj[m0 * cols + c], proj[m1 * cols + c], rp);
+    }
+}
+
+template <typename T, bool kMax>
+__global__ void combine_kernel(const T *__restrict__ src, T *__restrict__ dst, int64_t count) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = dst[e], b = src[e];
+        dst[e] = (T)(kMax ? max(a, b) : a + b);
+    }
+}
+
+unsigned grid_for(int64_t total, int threads) {
+    const int64_t b = (total + threads - 1) / threads;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms() * 16));
+}
+
+}  // namespace
+}  // namespace ssb
+
+using namespace ssb;
+
+extern "C" int ssb_version(void) { return SSB_VERSION; }
+
+extern "C" const char *ssb_last_error(void) { return ssb::g_error.c_str(); }
+
+extern "C" int64_t ssb_launch_count(void) { return ssb::g_launches.load(); }
+
+extern "C" int ssb_profile_enable(int32_t on) {
+    ssb::g_prof.on = on != 0;
+    return SSB_OK;
+}
+
+extern "C" int ssb_profile_read(double *total_ms, int64_t *launches) {
+    double sum = 0.0;
+    int64_t k = 0;
+    for (auto &pr : ssb::g_prof.pending) {
+        if (cudaEventSynchronize(pr.second) != cudaSuccess) return fail(SSB_ERR_CUDA, "profile event sync failed");
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) {
+            sum += ms;
+            ++k;
+        }
+        ssb::g_prof.pool.push_back(pr.first);
+        ssb::g_prof.pool.push_back(pr.second);
+    }
+    ssb::g_prof.pending.clear();
+    if (total_ms) *total_ms = sum;
+    if (launches) *launches = k;
+    return SSB_OK;
+}
+
+extern "C" int ssb_rolling_band(const uint16_t *ring, const uint8_t *present, int64_t n_ring,
+                                int64_t height, int64_t width, double shear_px, int32_t interp,
+                                int64_t lo, int64_t hi, uint16_t *canvas, int16_t *contributor,
+                                int64_t canvas_rows, void *stream) {
+    if (n_ring < 1 || height < 1 || width < 1) return fail(SSB_ERR_PARAM, "bad ring shape");
+    if (!(shear_px >= 0.0)) return fail(SSB_ERR_PARAM, "shear_px must be >= 0");
+    if (interp != SSB_INTERP_NEAREST && interp != SSB_INTERP_LINEAR)
+        return fail(SSB_ERR_PARAM, "interp must be nearest or linear");
+    if (lo < 0 || hi >= canvas_rows) return fail(SSB_ERR_CAPACITY, "band %lld..%lld outside %lld-row canvas",
+                                                (long long)lo, (long long)hi, (long long)canvas_rows);
+    if (hi < lo) return SSB_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t total = (hi - lo + 1) * width;
+    if (interp == SSB_INTERP_NEAREST)
+        rolling_band_kernel<SSB_INTERP_NEAREST><<<grid_for(total, 256), 256, 0, st>>>(
+            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor);
+    else
+        rolling_band_kernel<SSB_INTERP_LINEAR><<<grid_for(total, 256), 256, 0, st>>>(
+            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor);
+    count_launches(1);
+    return check_launch("rolling_band_kernel");
+}
+
+extern "C" int ssb_warp_rows(const uint16_t *proj, int64_t rows, int64_t cols, double warp_scale,
+                             uint16_t *out, int64_t out_rows, void *stream) {
+    if (!(warp_scale > 0.0)) return fail(SSB_ERR_PARAM, "warp_scale must be > 0, got %g", warp_scale);
+    if (rows < 1 || cols < 0 || out_rows < 1) return fail(SSB_ERR_PARAM, "bad warp shape");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (warp_scale == 1.0) {
+        if (out_rows != rows) return fail(SSB_ERR_PARAM, "identity warp must keep the row count");
+        cudaMemcpyAsync(out, proj, (size_t)rows * cols * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st);
+        return check_launch("ssb_warp_rows(copy)");
+    }
+    const int64_t total = out_rows * cols;
+    if (total == 0) return SSB_OK;
+    warp_rows_kernel<<<grid_for(total, 256), 256, 0, st>>>(proj, rows, cols, warp_scale, out, out_rows);
+    count_launches(1);
+    return check_launch("warp_rows_kernel");
+}
+
+extern "C" int ssb_combine(const void *src, void *dst, int64_t count, int32_t reduce, int32_t elem_bits,
+                           void *stream) {
+    if (count < 0) return fail(SSB_ERR_PARAM, "negative count");
+    if (count == 0) return SSB_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (elem_bits == 16 && reduce == SSB_REDUCE_MAX)
+        combine_kernel<uint16_t, true><<<grid_for(count, 256), 256, 0, st>>>(
+            static_cast<const uint16_t *>(src), static_cast<uint16_t *>(dst), count);
+    else if (elem_bits == 32 && reduce == SSB_REDUCE_MAX)
+        combine_kernel<uint32_t, true><<<grid_for(count, 256), 256, 0, st>>>(
+            static_cast<const uint32_t *>(src), static_cast<uint32_t *>(dst), count);
+    else if (elem_bits == 32 && reduce == SSB_REDUCE_SUM)
+        combine_kernel<uint32_t, false><<<grid_for(count, 256), 256, 0, st>>>(
+            static_cast<const uint32_t *>(src), static_cast<uint32_t *>(dst), count);
+    else
+        return fail(SSB_ERR_PARAM, "combine supports u16 max, u32 max, u32 sum");
+    count_launches(1);
+    return check_launch("combine_kernel");
+}

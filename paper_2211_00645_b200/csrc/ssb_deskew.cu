@@ -1,0 +1,382 @@
+// Fused deskew + XY/XZ/YZ projections (ssb_deskew) -- tiled path.
+//
+// Replaces the reference's per-frame numpy loop (ProjectionCanvas.place x N +
+// finalize_global, ss/pipeline.py:316-336; _interp_slice_rows :229-236) and the
+// batch oracle reference_deskew (ss/phantom.py:359-402) with one pass over HBM:
+// every raw frame row is read once (+1 halo row per tile), every volume voxel is
+// written once, and the projections are reduced on chip.
+//
+// Work decomposition: an item is (u-tile of TU canvas rows) x (x-tile of 256
+// columns) x (chunk of slices).  A 256-thread CTA = 8 warps; warp w owns ROWS
+// consecutive canvas rows, lane l owns 8 consecutive columns (16-byte vectors).
+// For each slice of the chunk the CTA
+//   * samples the frame (nearest copy or fp64 lerp, bit-exact with numpy),
+//   * streams the voxels to the volume (st.global.cs, 512 B per warp-row),
+//   * folds them into the XY accumulators held in registers (reduce over i),
+//   * reduces each row over its 256 columns with REDUX (YZ partial per x-tile),
+//   * reduces each column over its TU rows through shared memory (XZ partial
+//     per u-tile).
+// Partials of XY (per slice chunk), XZ (per u-tile) and YZ (per x-tile) land in
+// the workspace and one small kernel folds them; when a dimension has a single
+// partial the kernel writes the final projection directly.
+#include <algorithm>
+#include <cstring>
+
+#include "ssb_common.cuh"
+#include "ssb_host.h"
+
+namespace ssb {
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kTX = 256;  // columns per tile: 32 lanes x 8
+
+struct TileParams {
+    const uint16_t *raw;
+    uint16_t *vol;
+    void *xy;  // base of XY planes (S planes of u_count*W), or final
+    void *xz;  // base of XZ planes (UT planes of n*W), or final
+    void *yz;  // base of YZ planes (XT planes of n*u_count), or final
+    int64_t n, h, w, first, u_begin, u_count, chunk;
+    double shear;
+    int32_t UT, XT, S;
+    int32_t xy_accumulate;
+};
+
+template <bool VEC>
+__device__ __forceinline__ uint4 load8(const uint16_t *row, int64_t x, int64_t w) {
+    if (VEC) return ldg_nc_v4(row + x);
+    uint32_t v[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        if (x + c < w) v[c >> 1] |= (uint32_t)__ldg(row + x + c) << (16 * (c & 1));
+    return make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+template <bool VEC>
+__device__ __forceinline__ void store8(uint16_t *row, int64_t x, int64_t w, uint4 v) {
+    if (VEC) {
+        stg_cs_v4(row + x, v);
+        return;
+    }
+    const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        if (x + c < w) row[x + c] = (uint16_t)(q[c >> 1] >> (16 * (c & 1)));
+}
+
+template <int ROWS, int INTERP, int FORMULA, int REDUCE, bool VEC>
+__global__ void __launch_bounds__(kThreads) deskew_tiles_kernel(const TileParams p) {
+    constexpr int TU = kWarps * ROWS;
+    constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
+    __shared__ uint32_t xz_smem[kWarps][kTX];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int64_t item = blockIdx.x;
+    const int sc = (int)(item % p.S);
+    item /= p.S;
+    const int xt = (int)(item % p.XT);
+    const int ut = (int)(item / p.XT);
+
+    const int64_t x = (int64_t)xt * kTX + lane * 8;
+    const bool col_ok = x < p.w;
+    const int64_t r0 = (int64_t)ut * TU + warp * ROWS;  // first row (within window) of this warp
+    const int64_t tile_u0 = p.u_begin + (int64_t)ut * TU;
+    const int64_t tile_u1 = tile_u0 + TU - 1;
+    const int64_t s_begin = (int64_t)sc * p.chunk;
+    const int64_t s_end = min(p.n, s_begin + p.chunk);
+    const size_t frame_elems = (size_t)p.h * (size_t)p.w;
+
+    // XY accumulators: max -> 8 packed uint16 per row; sum -> 8 uint32 per row
+    uint4 acc_max[ROWS];
+    uint32_t acc_sum[kMax ? 1 : ROWS][8];
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+        acc_max[k] = make_uint4(0, 0, 0, 0);
+        if (!kMax)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc_sum[k][c] = 0;
+    }
+
+    for (int64_t s = s_begin; s < s_end; ++s) {
+        const int64_t gi = p.first + s;
+        int64_t lo, hi;
+        double off;
+        slice_span(gi, p.shear, p.h, INTERP, lo, hi, off);
+        const bool touches = !(hi < tile_u0 || lo > tile_u1);
+        const uint16_t *frame = p.raw + (size_t)s * frame_elems;
+
+        // lane k < ROWS derives the sampling parameters of row r0 + k
+        RowParam mine;
+        mine.kind = 0;
+        mine.j0 = mine.j1 = 0;
+        mine.c0 = 0.0;
+        mine.c1 = 1.0;
+        if (touches && lane < ROWS) {
+            const int64_t r = r0 + lane;
+            const int64_t u = p.u_begin + r;
+            if (r < p.u_count && u >= lo && u <= hi) mine = row_param<INTERP, FORMULA>(u, lo, off, p.h);
+        }
+
+        uint4 xz_max = make_uint4(0, 0, 0, 0);
+        uint32_t xz_sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+#pragma unroll
+        for (int k = 0; k < ROWS; ++k) {
+            RowParam rp;
+            rp.kind = __shfl_sync(0xffffffffu, mine.kind, k);
+            rp.j0 = __shfl_sync(0xffffffffu, mine.j0, k);
+            rp.j1 = __shfl_sync(0xffffffffu, mine.j1, k);
+            if (INTERP == SSB_INTERP_LINEAR) {
+                rp.c0 = __shfl_sync(0xffffffffu, mine.c0, k);
+                rp.c1 = __shfl_sync(0xffffffffu, mine.c1, k);
+            }
+            const int64_t r = r0 + k;
+            const bool row_ok = r < p.u_count;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (rp.kind != 0 && col_ok) {
+                const uint4 a = load8<VEC>(frame + (size_t)rp.j0 * p.w, x, p.w);
+                if (rp.kind == 1) {
+                    v = a;
+                } else {
+                    const uint4 b = load8<VEC>(frame + (size_t)rp.j1 * p.w, x, p.w);
+                    v = lerp8<FORMULA>(a, b, rp);
+                }
+            }
+            if (p.vol != nullptr && row_ok && col_ok)
+                store8<VEC>(p.vol + ((size_t)s * p.u_count + r) * p.w, x, p.w, v);
+            if (kMax) {
+                acc_max[k] = max_u16x8(acc_max[k], v);
+                xz_max = max_u16x8(xz_max, v);
+            } else {
+                const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t e = (q[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                    acc_sum[k][c] += e;
+                    xz_sum[c] += e;
+                }
+            }
+            if (p.yz != nullptr) {
+                const uint32_t part = kMax ? hmax_u16x8(v) : hsum_u16x8(v);
+                const uint32_t red = kMax ? __reduce_max_sync(0xffffffffu, part)
+                                          : __reduce_add_sync(0xffffffffu, part);
+                if (lane == 0 && row_ok) {
+                    const size_t idx = (size_t)xt * p.n * p.u_count + (size_t)s * p.u_count + r;
+                    if (kMax) static_cast<uint16_t *>(p.yz)[idx] = (uint16_t)red;
+                    else static_cast<uint32_t *>(p.yz)[idx] = red;
+                }
+            }
+        }
+
+        if (p.xz != nullptr) {
+            // column partial over this warp's rows -> smem -> reduce over warps
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t e;
+                if (kMax) {
+                    const uint32_t q[4] = {xz_max.x, xz_max.y, xz_max.z, xz_max.w};
+                    e = (q[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                } else {
+                    e = xz_sum[c];
+                }
+                xz_smem[warp][lane * 8 + c] = e;
+            }
+            __syncthreads();
+            const int64_t col = (int64_t)xt * kTX + tid;
+            if (col < p.w) {
+                uint32_t red = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) red = kMax ? max(red, xz_smem[w][tid]) : red + xz_smem[w][tid];
+                const size_t idx = (size_t)ut * p.n * p.w + (size_t)s * p.w + col;
+                if (kMax) static_cast<uint16_t *>(p.xz)[idx] = (uint16_t)red;
+                else static_cast<uint32_t *>(p.xz)[idx] = red;
+            }
+            __syncthreads();
+        }
+    }
+
+    if (p.xy == nullptr || !col_ok) return;
+    const size_t plane = (size_t)p.u_count * p.w;
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+        const int64_t r = r0 + k;
+        if (r >= p.u_count) break;
+        const size_t base = (size_t)sc * plane + (size_t)r * p.w + x;
+        if (kMax) {
+            uint16_t *dst = static_cast<uint16_t *>(p.xy) + base;
+            uint4 v = acc_max[k];
+            if (p.xy_accumulate) v = max_u16x8(v, load8<VEC>(dst, 0, p.w - x));
+            store8<VEC>(dst, 0, p.w - x, v);
+        } else {
+            uint32_t *dst = static_cast<uint32_t *>(p.xy) + base;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (x + c >= p.w) break;
+                dst[c] = p.xy_accumulate ? dst[c] + acc_sum[k][c] : acc_sum[k][c];
+            }
+        }
+    }
+}
+
+// dst[m] = reduce_p src[p*M + m] (optionally also over the old dst[m])
+template <typename T, bool kMax>
+__global__ void reduce_planes_kernel(const T *__restrict__ src, T *__restrict__ dst, int64_t planes,
+                                     int64_t m_total, int accumulate) {
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < m_total;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = accumulate ? (uint32_t)dst[m] : 0u;
+        for (int64_t q = 0; q < planes; ++q) {
+            const uint32_t e = (uint32_t)src[q * m_total + m];
+            v = kMax ? max(v, e) : v + e;
+        }
+        dst[m] = (T)v;
+    }
+}
+
+struct Plan {
+    int rows;        // rows per warp
+    int64_t TU, UT, XT, S, chunk;
+    size_t esz;      // bytes per projection element
+    size_t xy_ws, xz_ws, yz_ws;  // workspace bytes per partial kind (0 = direct)
+};
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+Plan make_plan(const ssb_deskew_desc &d, bool want_xy, bool want_xz, bool want_yz) {
+    Plan pl{};
+    pl.rows = d.reduce == SSB_REDUCE_MAX ? 8 : 4;
+    pl.TU = kWarps * pl.rows;
+    pl.UT = std::max<int64_t>(1, (d.u_count + pl.TU - 1) / pl.TU);
+    pl.XT = std::max<int64_t>(1, (d.width + kTX - 1) / kTX);
+    const int64_t resident = (int64_t)num_sms() * 4;
+    const int64_t tiles = pl.UT * pl.XT;
+    pl.S = std::min<int64_t>(std::max<int64_t>(1, (4 * resident + tiles - 1) / tiles), std::max<int64_t>(1, d.n));
+    if (d.flags & SSB_FLAG_XY_ACCUMULATE) pl.S = std::min<int64_t>(pl.S, 8);
+    pl.chunk = (d.n + pl.S - 1) / pl.S;
+    if (pl.chunk < 1) pl.chunk = 1;
+    pl.S = (d.n + pl.chunk - 1) / pl.chunk;
+    if (pl.S < 1) pl.S = 1;
+    pl.esz = d.reduce == SSB_REDUCE_MAX ? 2 : 4;
+    pl.xy_ws = (want_xy && pl.S > 1) ? align_up((size_t)pl.S * d.u_count * d.width * pl.esz) : 0;
+    pl.xz_ws = (want_xz && pl.UT > 1) ? align_up((size_t)pl.UT * d.n * d.width * pl.esz) : 0;
+    pl.yz_ws = (want_yz && pl.XT > 1) ? align_up((size_t)pl.XT * d.n * d.u_count * pl.esz) : 0;
+    return pl;
+}
+
+int validate(const ssb_deskew_desc *d) {
+    if (d == nullptr) return fail(SSB_ERR_PARAM, "null descriptor");
+    if (d->n < 0 || d->height < 1 || d->width < 1)
+        return fail(SSB_ERR_PARAM, "bad stack shape n=%lld H=%lld W=%lld", (long long)d->n,
+                    (long long)d->height, (long long)d->width);
+    if (!(d->shear_px >= 0.0)) return fail(SSB_ERR_PARAM, "shear_px must be >= 0, got %g", d->shear_px);
+    if (d->interp != SSB_INTERP_NEAREST && d->interp != SSB_INTERP_LINEAR)
+        return fail(SSB_ERR_PARAM, "interp must be nearest or linear");
+    if (d->formula != SSB_FORMULA_CANVAS && d->formula != SSB_FORMULA_NPINTERP)
+        return fail(SSB_ERR_PARAM, "unknown formula %d", d->formula);
+    if (d->reduce != SSB_REDUCE_MAX && d->reduce != SSB_REDUCE_SUM)
+        return fail(SSB_ERR_PARAM, "reduce must be max or sum");
+    if (d->u_count < 0 || d->u_begin < 0) return fail(SSB_ERR_PARAM, "bad canvas row window");
+    if (d->height > INT32_MAX) return fail(SSB_ERR_CAPACITY, "frame height too large");
+    return SSB_OK;
+}
+
+template <int ROWS, int INTERP, int FORMULA, int REDUCE>
+void launch_tiles(const TileParams &tp, int64_t items, bool vec, cudaStream_t st) {
+    if (vec) deskew_tiles_kernel<ROWS, INTERP, FORMULA, REDUCE, true><<<(unsigned)items, kThreads, 0, st>>>(tp);
+    else deskew_tiles_kernel<ROWS, INTERP, FORMULA, REDUCE, false><<<(unsigned)items, kThreads, 0, st>>>(tp);
+}
+
+template <int REDUCE>
+void dispatch_interp(const ssb_deskew_desc &d, const TileParams &tp, int64_t items, bool vec,
+                     cudaStream_t st) {
+    constexpr int R = REDUCE == SSB_REDUCE_MAX ? 8 : 4;
+    if (d.interp == SSB_INTERP_NEAREST)
+        launch_tiles<R, SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, REDUCE>(tp, items, vec, st);
+    else if (d.formula == SSB_FORMULA_CANVAS)
+        launch_tiles<R, SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, REDUCE>(tp, items, vec, st);
+    else
+        launch_tiles<R, SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, REDUCE>(tp, items, vec, st);
+}
+
+void launch_reduce(const void *src, void *dst, int64_t planes, int64_t m, bool is_max, bool accumulate,
+                   cudaStream_t st) {
+    if (m <= 0) return;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>((m + threads - 1) / threads, (int64_t)num_sms() * 8);
+    if (is_max)
+        reduce_planes_kernel<uint16_t, true><<<(unsigned)blocks, threads, 0, st>>>(
+            static_cast<const uint16_t *>(src), static_cast<uint16_t *>(dst), planes, m, accumulate);
+    else
+        reduce_planes_kernel<uint32_t, false><<<(unsigned)blocks, threads, 0, st>>>(
+            static_cast<const uint32_t *>(src), static_cast<uint32_t *>(dst), planes, m, accumulate);
+    count_launches(1);
+}
+
+}  // namespace
+}  // namespace ssb
+
+using namespace ssb;
+
+extern "C" size_t ssb_deskew_workspace_bytes(const ssb_deskew_desc *d) {
+    if (validate(d) != SSB_OK) return 0;
+    const Plan pl = make_plan(*d, true, true, true);
+    return pl.xy_ws + pl.xz_ws + pl.yz_ws + 256;
+}
+
+extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_t *vol, void *xy,
+                          void *xz, void *yz, void *workspace, size_t workspace_bytes, void *stream) {
+    if (int rc = validate(d)) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (d->n == 0 || d->u_count == 0) {
+        // nothing placed: projections of an empty window are zero (XY unless accumulating)
+        const size_t esz = d->reduce == SSB_REDUCE_MAX ? 2 : 4;
+        if (xy && !(d->flags & SSB_FLAG_XY_ACCUMULATE))
+            cudaMemsetAsync(xy, 0, (size_t)d->u_count * d->width * esz, st);
+        return check_launch("ssb_deskew(empty)");
+    }
+    if (raw == nullptr) return fail(SSB_ERR_PARAM, "raw frames pointer is null");
+    const Plan pl = make_plan(*d, xy != nullptr, xz != nullptr, yz != nullptr);
+    const size_t need = pl.xy_ws + pl.xz_ws + pl.yz_ws;
+    if (need > 0 && (workspace == nullptr || workspace_bytes < need))
+        return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
+
+    char *ws = static_cast<char *>(workspace);
+    TileParams tp{};
+    tp.raw = raw;
+    tp.vol = vol;
+    tp.xy = pl.xy_ws ? (void *)ws : xy;
+    tp.xz = pl.xz_ws ? (void *)(ws + pl.xy_ws) : xz;
+    tp.yz = pl.yz_ws ? (void *)(ws + pl.xy_ws + pl.xz_ws) : yz;
+    tp.n = d->n;
+    tp.h = d->height;
+    tp.w = d->width;
+    tp.first = d->first_slice;
+    tp.u_begin = d->u_begin;
+    tp.u_count = d->u_count;
+    tp.chunk = pl.chunk;
+    tp.shear = d->shear_px;
+    tp.UT = (int32_t)pl.UT;
+    tp.XT = (int32_t)pl.XT;
+    tp.S = (int32_t)pl.S;
+    tp.xy_accumulate = (pl.xy_ws == 0 && (d->flags & SSB_FLAG_XY_ACCUMULATE)) ? 1 : 0;
+
+    const bool vec = (d->width % 8 == 0) && aligned16(raw) && aligned16(vol) &&
+                     (d->reduce != SSB_REDUCE_MAX || aligned16(tp.xy));
+    const int64_t items = pl.UT * pl.XT * pl.S;
+    if (items > INT32_MAX) return fail(SSB_ERR_CAPACITY, "too many tiles");
+    profile_begin(st);
+    if (d->reduce == SSB_REDUCE_MAX) dispatch_interp<SSB_REDUCE_MAX>(*d, tp, items, vec, st);
+    else dispatch_interp<SSB_REDUCE_SUM>(*d, tp, items, vec, st);
+    profile_end(st);
+    count_launches(1);
+    if (int rc = check_launch("deskew_tiles_kernel")) return rc;
+
+    const bool is_max = d->reduce == SSB_REDUCE_MAX;
+    if (pl.xy_ws) launch_reduce(tp.xy, xy, pl.S, d->u_count * d->width, is_max,
+                                (d->flags & SSB_FLAG_XY_ACCUMULATE) != 0, st);
+    if (pl.xz_ws) launch_reduce(tp.xz, xz, pl.UT, d->n * d->width, is_max, false, st);
+    if (pl.yz_ws) launch_reduce(tp.yz, yz, pl.XT, d->n * d->u_count, is_max, false, st);
+    return check_launch("reduce_planes_kernel");
+}

@@ -1,0 +1,35 @@
+"""Error classes of the drop-in, one per reference class.
+
+Mirrors ``skewstream/errors.py:4-25`` so callers that catch the reference's
+exceptions (``except ParameterError`` / ``pytest.raises(CapacityError)``)
+keep working. C-ABI status codes (``include/ssb.h``) map onto these in
+``paper_2211_00645_b200._lib``.
+"""
+
+
+class SkewstreamError(Exception):
+    """Root of every error raised by this package (ss/errors.py:4)."""
+
+
+class ParameterError(SkewstreamError, ValueError):
+    """Out-of-range or malformed argument (ss/errors.py:8)."""
+
+
+class CapacityError(SkewstreamError):
+    """A canvas or buffer limit would be exceeded (ss/errors.py:12)."""
+
+
+class ProtocolError(SkewstreamError):
+    """Call made out of sequence, e.g. finalize before a full sweep (ss/errors.py:16)."""
+
+
+class MetadataError(SkewstreamError):
+    """Stack metadata missing or inconsistent (ss/errors.py:20)."""
+
+
+class EndOfStream(SkewstreamError):
+    """A finite frame source ran dry (ss/errors.py:24)."""
+
+
+class DeviceError(SkewstreamError):
+    """A CUDA call failed, or the native library is missing on a GPU box."""

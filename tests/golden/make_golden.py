@@ -1,0 +1,206 @@
+"""Generate golden fixtures by running the REFERENCE implementation itself.
+
+Run here (the reference is importable only in the build container):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It writes small ``.npz`` fixtures next to this file.  Nothing at test time
+reads ``/root/reference``; the fixtures travel with the repo.
+
+Sources of truth (reference file:line):
+* geometry tables: ``geometry.output_extent`` / ``nearest_offset`` /
+  ``linear_row_span`` (ss/geometry.py:129-147, 236-255)
+* streaming rows + canvas: ``ProjectionCanvas.row_span`` / ``_slice_rows`` /
+  ``place`` / ``finalize_global`` (ss/pipeline.py:274-336) -- the per-slice
+  rows give the deskewed volume V[i, lo:hi+1] exactly as the reference
+  computes them; the canvas is its axis-0 max
+* batch rows: ``phantom.reference_deskew`` (ss/phantom.py:359-402) on one-hot
+  stacks (all frames zero but frame i) gives slice i's rounded np.interp rows;
+  the full call gives the batch MIP
+* warp: ``pipeline.warp_projection`` (ss/pipeline.py:434-457)
+* rolling: ``ProjectionCanvas.rolling_replace`` / ``replace_all``
+  (ss/pipeline.py:345-398) snapshots of ``max_pixels`` and ``contributor``
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+from skewstream import geometry as G
+from skewstream import phantom as PH
+from skewstream import pipeline as PL
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def geom(n, h, w, alpha=60.0, step=0.2, pitch=0.1):
+    return G.SheetGeometry(alpha_deg=alpha, scan_step_um=step, pixel_pitch_um=pitch,
+                           slice_count=n, frame_width_px=w, frame_height_px=h)
+
+
+def canvas_case(stack, s, interp):
+    n, h, w = stack.shape
+    g = geom(n, h, w)
+    c = PL.ProjectionCanvas(g, s, interp=interp)
+    vol = np.zeros((n, c.height, w), dtype=np.uint16)
+    spans = np.zeros((n, 2), dtype=np.int64)
+    for i in range(n):
+        f = PL.RawFrame(stack[i], i)
+        lo, hi = c.row_span(i)
+        spans[i] = (lo, hi)
+        vol[i, lo:hi + 1] = c._slice_rows(f, lo, hi)
+        c.place(f)
+    xy = c.finalize_global()
+    return vol, xy, spans
+
+
+def batch_case(stack, s, interp):
+    n, h, w = stack.shape
+    g = geom(n, h, w)
+    full = PH.reference_deskew(list(stack), g, s, interp=interp)
+    vol = np.zeros((n,) + full.shape, dtype=np.uint16)
+    for i in range(n):
+        onehot = np.zeros_like(stack)
+        onehot[i] = stack[i]
+        vol[i] = PH.reference_deskew(list(onehot), g, s, interp=interp)
+    # the one-hot trick is exact only where slice i is the unique nonzero
+    # contributor; restrict the volume golden to slice i's own span
+    for i in range(n):
+        if interp == "nearest":
+            lo = G.nearest_offset(i, s)
+            hi = lo + h - 1
+        else:
+            lo, hi = G.linear_row_span(i, s, h)
+        vol[i, :max(lo, 0)] = 0
+        vol[i, hi + 1:] = 0
+    return vol, full
+
+
+def main():
+    rng = np.random.default_rng(20221101)
+    out = {}
+
+    # ---- geometry tables -------------------------------------------------
+    shears = np.concatenate([
+        rng.uniform(0.0, 3.0, 200),
+        np.array([0.0, 0.5, 1.0, 2.0, 1.5, 0.1 * 3, 0.7 + 1e-12, 1.0 - 1e-12,
+                  1.0 + 1e-10, 2.0 / 3.0, 1.0 / 3.0, np.cos(np.radians(30.0)),
+                  np.cos(np.radians(45.0)), 0.866025403784439, 0.25, 0.125]),
+    ])
+    idx = np.concatenate([np.arange(0, 160), np.arange(500, 520), np.arange(8180, 8192)])
+    hs = np.array([1, 2, 3, 7, 256, 2048])
+    tab_lin = np.zeros((shears.size, idx.size, hs.size, 2), dtype=np.int64)
+    tab_near = np.zeros((shears.size, idx.size), dtype=np.int64)
+    for a, s in enumerate(shears):
+        for b, i in enumerate(idx):
+            tab_near[a, b] = G.nearest_offset(int(i), float(s))
+            for c, h in enumerate(hs):
+                tab_lin[a, b, c] = G.linear_row_span(int(i), float(s), int(h))
+    ns = np.array([1, 2, 5, 128, 200, 512, 8192])
+    ext = np.zeros((shears.size, ns.size, hs.size), dtype=np.int64)
+    for a, s in enumerate(shears):
+        for b, n in enumerate(ns):
+            for c, h in enumerate(hs):
+                ext[a, b, c] = G.output_extent(geom(int(n), int(h), 4), float(s),
+                                               max_pixels=10**15)[1]
+    np.savez_compressed(os.path.join(HERE, "geometry.npz"), shears=shears, idx=idx,
+                        hs=hs, ns=ns, linear_span=tab_lin, nearest_off=tab_near,
+                        extent_height=ext)
+
+    # ---- volume / canvas / batch cases -----------------------------------
+    cases = []
+    # (n, h, w, s, interp, hi_value)
+    base = [
+        (2, 2, 2, 1.0, "nearest", 10),
+        (3, 2, 2, 1.0, "nearest", 10),
+        (2, 2, 2, 0.5, "linear", 4),
+        (2, 2, 2, 0.5, "nearest", 4),
+        (4, 4, 3, 2.0, "linear", 65536),
+        (5, 4, 6, 1.6, "nearest", 4096),
+        (5, 4, 3, 1.3, "linear", 65536),
+        (1, 4, 3, 1.5, "linear", 65536),
+        (6, 1, 5, 0.7, "linear", 65536),
+        (6, 5, 1, 0.7, "linear", 65536),
+        (7, 9, 17, 0.0, "linear", 65536),
+        (7, 9, 17, 0.0, "nearest", 65536),
+        (9, 12, 33, 0.5, "linear", 8),     # exact half ties -> rint half-even
+        (9, 12, 33, 0.25, "linear", 65536),
+        (16, 32, 40, 1.0 + 1e-10, "linear", 65536),   # offsets within 1e-9 of integers
+        (16, 32, 40, 1.0 - 1e-12, "linear", 65536),
+        (16, 32, 40, 0.1 * 3, "linear", 65536),
+        (16, 32, 40, 2.0 / 3.0, "linear", 65536),
+        (16, 32, 40, 2.0 / 3.0, "nearest", 65536),
+        (20, 24, 72, float(np.cos(np.radians(30.0))), "linear", 4096),
+        (20, 24, 72, float(np.cos(np.radians(30.0))), "nearest", 4096),
+        (20, 24, 72, float(np.cos(np.radians(45.0))), "linear", 65536),
+        (12, 40, 136, 1.7320508075688772, "linear", 65536),  # 2x native at 30 deg
+        (33, 17, 64, 0.3660254037844386, "linear", 65536),
+        (24, 40, 264, 0.8660254037844386, "linear", 65536),  # ragged width (not /8)
+        (32, 48, 136, 0.8660254037844386, "linear", 4096),
+        (32, 48, 136, 0.8660254037844386, "nearest", 4096),
+    ]
+    for _ in range(14):
+        n = int(rng.integers(1, 24))
+        h = int(rng.integers(1, 40))
+        w = int(rng.integers(1, 70))
+        s = float(rng.uniform(0.0, 2.5))
+        cases.append((n, h, w, s, str(rng.choice(["nearest", "linear"])), 65536))
+    cases = base + cases
+
+    for k, (n, h, w, s, interp, vmax) in enumerate(cases):
+        stack = rng.integers(0, vmax, size=(n, h, w)).astype(np.uint16)
+        vol, xy, spans = canvas_case(stack, s, interp)
+        bvol, bxy = batch_case(stack, s, interp)
+        np.savez_compressed(os.path.join(HERE, f"case_{k:03d}.npz"),
+                            stack=stack, shear=np.float64(s), interp=interp,
+                            vol=vol, xy=xy, spans=spans, batch_vol=bvol, batch_xy=bxy)
+        print(f"case {k}: n={n} h={h} w={w} s={s!r} {interp} canvas={xy.shape}", file=sys.stderr)
+
+    # ---- warp ---------------------------------------------------------------
+    warp = {}
+    for k, (rows, cols, scale) in enumerate([(4, 3, 1.0), (2, 1, 2.0), (4, 1, 0.5),
+                                              (37, 11, 1.3), (64, 9, 0.77), (50, 5, 0.9999),
+                                              (91, 64, 1.1547005383792517)]):
+        proj = rng.integers(0, 65536, size=(rows, cols)).astype(np.uint16)
+        warp[f"in_{k}"] = proj
+        warp[f"scale_{k}"] = np.float64(scale)
+        warp[f"out_{k}"] = PL.warp_projection(proj, scale)
+    np.savez_compressed(os.path.join(HERE, "warp.npz"), **warp)
+
+    # ---- rolling ------------------------------------------------------------
+    roll = {}
+    k = 0
+    for (n, h, w, s, interp) in [(5, 4, 3, 1.3, "linear"), (2, 2, 2, 1.0, "nearest"),
+                                 (8, 12, 10, 0.5773502691896258, "linear"),
+                                 (8, 12, 10, 1.37, "nearest"), (6, 7, 9, 0.0, "linear")]:
+        g = geom(n, h, w)
+        c = PL.ProjectionCanvas(g, s, interp=interp, mode="rolling")
+        frames = []
+        # two full sweeps then a partial third, with a shear change in between
+        for sweep in range(3):
+            order = rng.permutation(n) if sweep == 1 else np.arange(n)
+            for i in order[: (n if sweep < 2 else max(1, n // 2))]:
+                px = rng.integers(0, 65536, size=(h, w)).astype(np.uint16)
+                frames.append((int(i), px))
+                c.rolling_replace(PL.RawFrame(px, int(i), sweep_index=sweep))
+                roll[f"c{k}_step{len(frames) - 1}_max"] = c.max_pixels.copy()
+                roll[f"c{k}_step{len(frames) - 1}_contrib"] = c.contributor.copy()
+        c.replace_all(s * 1.5 + 0.1)
+        roll[f"c{k}_after_replace_max"] = c.max_pixels.copy()
+        roll[f"c{k}_after_replace_contrib"] = c.contributor.copy()
+        roll[f"c{k}_meta"] = np.array([n, h, w], dtype=np.int64)
+        roll[f"c{k}_shear"] = np.float64(s)
+        roll[f"c{k}_shear2"] = np.float64(s * 1.5 + 0.1)
+        roll[f"c{k}_interp"] = interp
+        roll[f"c{k}_slices"] = np.array([f[0] for f in frames], dtype=np.int64)
+        roll[f"c{k}_frames"] = np.stack([f[1] for f in frames])
+        k += 1
+    roll["count"] = np.int64(k)
+    np.savez_compressed(os.path.join(HERE, "rolling.npz"), **roll)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,109 @@
+"""Host-side contract of the drop-in that runs without a GPU: frame/channel types,
+argument validation (same exceptions and messages as the reference) and the
+no-fallback rule (compute entry points raise instead of running on the CPU)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2211_00645_b200 import pipeline as pl
+from paper_2211_00645_b200.errors import (CapacityError, DeviceError, ParameterError,
+                                          SkewstreamError)
+from ssb_testutil import geom
+
+NO_GPU = not torch.cuda.is_available()
+
+
+def frame(arr, i, **kw):
+    return pl.RawFrame(np.asarray(arr, dtype=np.uint16), i, **kw)
+
+
+class TestRawFrame:  # pkg/tests/test_pipeline.py:44-61
+    def test_requires_uint16(self):
+        with pytest.raises(ParameterError):
+            pl.RawFrame(np.zeros((2, 2), np.float32), 0)
+
+    def test_requires_2d(self):
+        with pytest.raises(ParameterError):
+            pl.RawFrame(np.zeros((2, 2, 2), np.uint16), 0)
+
+    def test_negative_slice(self):
+        with pytest.raises(ParameterError):
+            pl.RawFrame(np.zeros((2, 2), np.uint16), -1)
+
+    def test_shape(self):
+        f = frame(np.zeros((3, 5)), 0)
+        assert (f.height, f.width) == (3, 5)
+
+
+class TestChannels:  # pkg/tests/test_pipeline.py:64-103
+    def test_overlap_rejected(self):
+        with pytest.raises(ParameterError, match="overlap"):
+            pl.ChannelLayout(regions=(pl.ChannelRegion(0, 0, 0, 4, 4), pl.ChannelRegion(1, 2, 0, 4, 4)))
+
+    def test_split_two_channels(self):
+        layout = pl.ChannelLayout(regions=(pl.ChannelRegion(0, 0, 0, 2, 2), pl.ChannelRegion(1, 2, 0, 2, 2)))
+        f = frame([[1, 2, 3, 4], [5, 6, 7, 8]], 3, sweep_index=1)
+        subs = pl.split_channels(f, layout)
+        assert [s.channel_id for s in subs] == [0, 1]
+        np.testing.assert_array_equal(subs[0].pixels, [[1, 2], [5, 6]])
+        np.testing.assert_array_equal(subs[1].pixels, [[3, 4], [7, 8]])
+        subs[0].pixels[0, 0] = 99
+        assert f.pixels[0, 0] == 1
+
+    def test_region_exceeding_frame(self):
+        with pytest.raises(ParameterError):
+            pl.ChannelLayout(regions=(pl.ChannelRegion(0, 0, 0, 8, 8),)).validate_frame(4, 4)
+
+
+class TestValidationBeforeDevice:
+    def test_bad_interp_and_mode(self):  # pkg/tests/test_pipeline.py:216-222
+        with pytest.raises(ParameterError):
+            pl.ProjectionCanvas(geom(), 1.0, interp="cubic")
+        with pytest.raises(ParameterError):
+            pl.ProjectionCanvas(geom(), 1.0, mode="windowed")
+
+    def test_canvas_limit(self):
+        with pytest.raises(CapacityError):
+            pl.ProjectionCanvas(geom(n=100_000, w=10_000, h=10_000), 1.0)
+
+    def test_warp_bad_scale(self):  # pkg/tests/test_pipeline.py:296-302
+        proj = np.zeros((4, 2), np.uint16)
+        with pytest.raises(ParameterError):
+            pl.warp_projection(proj, 0.0)
+        with pytest.raises(ParameterError):
+            pl.warp_projection(proj, -1.0)
+
+    def test_reference_deskew_validation(self):  # pkg/tests/test_phantom.py:255-263
+        from paper_2211_00645_b200 import phantom as ph
+        with pytest.raises(ParameterError, match="frame 1"):
+            ph.reference_deskew([np.zeros((2, 2), np.uint16), np.zeros((3, 2), np.uint16)], geom(), 1.0)
+        with pytest.raises(ParameterError):
+            ph.reference_deskew([np.zeros((2, 2), np.uint16)], geom(), 1.0, interp="cubic")
+        with pytest.raises(ParameterError, match="empty"):
+            ph.reference_deskew([], geom(), 1.0)
+
+    def test_error_hierarchy(self):
+        assert issubclass(DeviceError, SkewstreamError)
+        assert issubclass(ParameterError, ValueError)
+
+
+@pytest.mark.skipif(not NO_GPU, reason="checks the no-fallback rule on a CPU-only host")
+class TestNoCpuFallback:
+    def test_canvas_needs_device(self):
+        with pytest.raises(DeviceError):
+            pl.ProjectionCanvas(geom(), 1.0)
+
+    def test_deskew_volume_needs_device(self):
+        from paper_2211_00645_b200.deskew import deskew_volume
+        with pytest.raises(DeviceError):
+            deskew_volume(np.zeros((2, 4, 8), np.uint16), geom(n=2, w=8, h=4), 1.0)
+
+    def test_deskew_device_rejects_host_tensor(self):
+        from paper_2211_00645_b200.deskew import deskew_device
+        with pytest.raises(ParameterError):
+            deskew_device(torch.zeros((2, 4, 8), dtype=torch.uint16), 1.0)
+
+    def test_warp_needs_device(self):
+        with pytest.raises(DeviceError):
+            pl.warp_projection(np.zeros((4, 2), np.uint16), 1.5)
