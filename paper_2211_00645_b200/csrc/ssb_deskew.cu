@@ -20,10 +20,12 @@
 // the workspace and one small kernel folds them; when a dimension has a single
 // partial the kernel writes the final projection directly.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "ssb_common.cuh"
 #include "ssb_host.h"
+#include "ssb_plan.h"
 
 namespace ssb {
 namespace {
@@ -236,34 +238,41 @@ __global__ void reduce_planes_kernel(const T *__restrict__ src, T *__restrict__ 
 }
 
 struct Plan {
-    int rows;        // rows per warp
     int64_t TU, UT, XT, S, chunk;
-    size_t esz;      // bytes per projection element
-    size_t xy_ws, xz_ws, yz_ws;  // workspace bytes per partial kind (0 = direct)
+    size_t esz;                  // bytes per projection element
+    size_t xy_ws, xz_ws, yz_ws;  // workspace bytes per partial kind (0 = written directly)
 };
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+constexpr size_t kCounterBytes = 256;  // scheduler counter at the head of the workspace
 
-Plan make_plan(const ssb_deskew_desc &d, bool want_xy, bool want_xz, bool want_yz) {
+int64_t env_int(const char *name, int64_t dflt) {
+    const char *v = getenv(name);
+    return v ? atoll(v) : dflt;
+}
+
+// tu: canvas rows per work item of the kernel that will run.
+Plan make_plan(const ssb_deskew_desc &d, bool want_xy, bool want_xz, bool want_yz, int64_t tu, bool persistent) {
     Plan pl{};
-    pl.rows = d.reduce == SSB_REDUCE_MAX ? 8 : 4;
-    pl.TU = kWarps * pl.rows;
-    pl.UT = std::max<int64_t>(1, (d.u_count + pl.TU - 1) / pl.TU);
+    pl.TU = tu;
+    pl.UT = std::max<int64_t>(1, (d.u_count + tu - 1) / tu);
     pl.XT = std::max<int64_t>(1, (d.width + kTX - 1) / kTX);
-    const int64_t resident = (int64_t)num_sms() * 4;
     const int64_t tiles = pl.UT * pl.XT;
-    pl.S = std::min<int64_t>(std::max<int64_t>(1, (4 * resident + tiles - 1) / tiles), std::max<int64_t>(1, d.n));
-    if (d.flags & SSB_FLAG_XY_ACCUMULATE) pl.S = std::min<int64_t>(pl.S, 8);
-    pl.chunk = (d.n + pl.S - 1) / pl.S;
-    if (pl.chunk < 1) pl.chunk = 1;
-    pl.S = (d.n + pl.chunk - 1) / pl.chunk;
-    if (pl.S < 1) pl.S = 1;
+    // enough items for the scheduler to balance: ~4 per resident CTA slot
+    const int64_t slots = (int64_t)num_sms() * (persistent ? 1 : 2);
+    int64_t S = std::max<int64_t>(1, (env_int("SSB_ITEMS_PER_SLOT", 4) * slots + tiles - 1) / tiles);
+    S = std::min<int64_t>(S, env_int("SSB_MAX_SLICE_CHUNKS", 8));
+    S = std::min<int64_t>(S, std::max<int64_t>(1, d.n));
+    pl.chunk = std::max<int64_t>(1, (d.n + S - 1) / S);
+    pl.S = std::max<int64_t>(1, (d.n + pl.chunk - 1) / pl.chunk);
     pl.esz = d.reduce == SSB_REDUCE_MAX ? 2 : 4;
     pl.xy_ws = (want_xy && pl.S > 1) ? align_up((size_t)pl.S * d.u_count * d.width * pl.esz) : 0;
     pl.xz_ws = (want_xz && pl.UT > 1) ? align_up((size_t)pl.UT * d.n * d.width * pl.esz) : 0;
     pl.yz_ws = (want_yz && pl.XT > 1) ? align_up((size_t)pl.XT * d.n * d.u_count * pl.esz) : 0;
     return pl;
 }
+
+int64_t tiled_rows(const ssb_deskew_desc &d) { return kWarps * (d.reduce == SSB_REDUCE_MAX ? 8 : 4); }
 
 int validate(const ssb_deskew_desc *d) {
     if (d == nullptr) return fail(SSB_ERR_PARAM, "null descriptor");
@@ -321,8 +330,9 @@ using namespace ssb;
 
 extern "C" size_t ssb_deskew_workspace_bytes(const ssb_deskew_desc *d) {
     if (validate(d) != SSB_OK) return 0;
-    const Plan pl = make_plan(*d, true, true, true);
-    return pl.xy_ws + pl.xz_ws + pl.yz_ws + 256;
+    const Plan a = make_plan(*d, true, true, true, kTmaTileRows, true);
+    const Plan b = make_plan(*d, true, true, true, tiled_rows(*d), false);
+    return kCounterBytes + std::max(a.xy_ws + a.xz_ws + a.yz_ws, b.xy_ws + b.xz_ws + b.yz_ws);
 }
 
 extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_t *vol, void *xy,
@@ -337,46 +347,62 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
         return check_launch("ssb_deskew(empty)");
     }
     if (raw == nullptr) return fail(SSB_ERR_PARAM, "raw frames pointer is null");
-    const Plan pl = make_plan(*d, xy != nullptr, xz != nullptr, yz != nullptr);
-    const size_t need = pl.xy_ws + pl.xz_ws + pl.yz_ws;
-    if (need > 0 && (workspace == nullptr || workspace_bytes < need))
+    const bool use_tma = env_int("SSB_DISABLE_TMA", 0) == 0 && tma_eligible(*d, raw, vol, xy);
+    const Plan pl = make_plan(*d, xy != nullptr, xz != nullptr, yz != nullptr,
+                              use_tma ? kTmaTileRows : tiled_rows(*d), use_tma);
+    const size_t need = kCounterBytes + pl.xy_ws + pl.xz_ws + pl.yz_ws;
+    if (workspace == nullptr || workspace_bytes < need)
         return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
 
     char *ws = static_cast<char *>(workspace);
-    TileParams tp{};
-    tp.raw = raw;
-    tp.vol = vol;
-    tp.xy = pl.xy_ws ? (void *)ws : xy;
-    tp.xz = pl.xz_ws ? (void *)(ws + pl.xy_ws) : xz;
-    tp.yz = pl.yz_ws ? (void *)(ws + pl.xy_ws + pl.xz_ws) : yz;
-    tp.n = d->n;
-    tp.h = d->height;
-    tp.w = d->width;
-    tp.first = d->first_slice;
-    tp.u_begin = d->u_begin;
-    tp.u_count = d->u_count;
-    tp.chunk = pl.chunk;
-    tp.shear = d->shear_px;
-    tp.UT = (int32_t)pl.UT;
-    tp.XT = (int32_t)pl.XT;
-    tp.S = (int32_t)pl.S;
-    tp.xy_accumulate = (pl.xy_ws == 0 && (d->flags & SSB_FLAG_XY_ACCUMULATE)) ? 1 : 0;
+    unsigned int *counters = reinterpret_cast<unsigned int *>(ws);
+    ws += kCounterBytes;
+    void *xy_dst = pl.xy_ws ? (void *)ws : xy;
+    void *xz_dst = pl.xz_ws ? (void *)(ws + pl.xy_ws) : xz;
+    void *yz_dst = pl.yz_ws ? (void *)(ws + pl.xy_ws + pl.xz_ws) : yz;
+    const int xy_acc = (pl.xy_ws == 0 && (d->flags & SSB_FLAG_XY_ACCUMULATE)) ? 1 : 0;
 
-    const bool vec = (d->width % 8 == 0) && aligned16(raw) && aligned16(vol) &&
-                     (d->reduce != SSB_REDUCE_MAX || aligned16(tp.xy));
-    const int64_t items = pl.UT * pl.XT * pl.S;
-    if (items > INT32_MAX) return fail(SSB_ERR_CAPACITY, "too many tiles");
-    profile_begin(st);
-    if (d->reduce == SSB_REDUCE_MAX) dispatch_interp<SSB_REDUCE_MAX>(*d, tp, items, vec, st);
-    else dispatch_interp<SSB_REDUCE_SUM>(*d, tp, items, vec, st);
-    profile_end(st);
-    count_launches(1);
-    if (int rc = check_launch("deskew_tiles_kernel")) return rc;
+    if (use_tma) {
+        profile_begin(st);
+        const int rc = launch_deskew_tma(*d, raw, vol, xy_dst, xz_dst, yz_dst, counters, pl.UT, pl.XT, pl.S,
+                                         pl.chunk, xy_acc, st);
+        profile_end(st);
+        if (rc) return rc;
+    } else {
+        TileParams tp{};
+        tp.raw = raw;
+        tp.vol = vol;
+        tp.xy = xy_dst;
+        tp.xz = xz_dst;
+        tp.yz = yz_dst;
+        tp.n = d->n;
+        tp.h = d->height;
+        tp.w = d->width;
+        tp.first = d->first_slice;
+        tp.u_begin = d->u_begin;
+        tp.u_count = d->u_count;
+        tp.chunk = pl.chunk;
+        tp.shear = d->shear_px;
+        tp.UT = (int32_t)pl.UT;
+        tp.XT = (int32_t)pl.XT;
+        tp.S = (int32_t)pl.S;
+        tp.xy_accumulate = xy_acc;
+        const bool vec = (d->width % 8 == 0) && aligned16(raw) && aligned16(vol) &&
+                         (d->reduce != SSB_REDUCE_MAX || aligned16(tp.xy));
+        const int64_t items = pl.UT * pl.XT * pl.S;
+        if (items > INT32_MAX) return fail(SSB_ERR_CAPACITY, "too many tiles");
+        profile_begin(st);
+        if (d->reduce == SSB_REDUCE_MAX) dispatch_interp<SSB_REDUCE_MAX>(*d, tp, items, vec, st);
+        else dispatch_interp<SSB_REDUCE_SUM>(*d, tp, items, vec, st);
+        profile_end(st);
+        count_launches(1);
+        if (int rc = check_launch("deskew_tiles_kernel")) return rc;
+    }
 
     const bool is_max = d->reduce == SSB_REDUCE_MAX;
-    if (pl.xy_ws) launch_reduce(tp.xy, xy, pl.S, d->u_count * d->width, is_max,
+    if (pl.xy_ws) launch_reduce(xy_dst, xy, pl.S, d->u_count * d->width, is_max,
                                 (d->flags & SSB_FLAG_XY_ACCUMULATE) != 0, st);
-    if (pl.xz_ws) launch_reduce(tp.xz, xz, pl.UT, d->n * d->width, is_max, false, st);
-    if (pl.yz_ws) launch_reduce(tp.yz, yz, pl.XT, d->n * d->u_count, is_max, false, st);
+    if (pl.xz_ws) launch_reduce(xz_dst, xz, pl.UT, d->n * d->width, is_max, false, st);
+    if (pl.yz_ws) launch_reduce(yz_dst, yz, pl.XT, d->n * d->u_count, is_max, false, st);
     return check_launch("reduce_planes_kernel");
 }

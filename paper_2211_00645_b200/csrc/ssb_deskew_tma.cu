@@ -1,0 +1,457 @@
+// Fused deskew + XY/XZ/YZ projections -- TMA-pipelined persistent kernel (sm_100a).
+//
+// Same contract and bit-exact arithmetic as the tiled path in ssb_deskew.cu
+// (ss/pipeline.py:229-236 canvas lerp, ss/phantom.py:396-402 np.interp lerp,
+// ss/geometry.py:236-255 spans), organised for B200:
+//
+//  * one persistent CTA per SM: 15 consumer warps + 1 producer warp;
+//  * the producer pulls work items from a global atomic counter (tiles ordered
+//    centre-out over the canvas rows, i.e. heaviest first), and for every slice
+//    that touches the tile issues one 3-D TMA box load (256 columns x TU+4 frame
+//    rows) into a 4-stage shared-memory ring guarded by full/empty mbarriers; its
+//    lanes also derive the per-row sampling parameters (fp64, once per row per
+//    slice instead of once per thread);
+//  * consumer warp w owns 4 canvas rows, lane l 8 columns: it reads the two frame
+//    rows of each canvas row from shared memory (conflict-free 512 B rows),
+//    evaluates 8 voxels with the exact fp64 expression, streams them to the volume
+//    with st.global.cs, and folds them into the XY (registers), YZ (REDUX) and
+//    XZ (shared memory, named barrier) reductions;
+//  * int->double conversion is folded into the products: fma(w, 2^52 + a,
+//    -w*2^52) == fl(w*a) exactly (one rounding), so a voxel costs 2 DFMA + 2 DADD.
+#include <algorithm>
+#include <cstring>
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "ssb_plan.h"
+
+#include "ssb_common.cuh"
+#include "ssb_host.h"
+#include "ssb_tma.cuh"
+
+namespace ssb {
+namespace tma_path {
+
+constexpr int kConsumerWarps = 15;  // + 1 producer = 16 warps: 128 registers per thread
+constexpr int kRows = 4;  // canvas rows per consumer warp
+constexpr int kTU = kConsumerWarps * kRows;
+constexpr int kBoxRows = kTU + 4;  // +2 rows of slack on each side of the tile
+constexpr int kTX = 256;
+constexpr int kStages = 4;
+constexpr int kQueue = 4;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kConsumerThreads = kConsumerWarps * 32;
+constexpr uint32_t kBoxBytes = kBoxRows * kTX * 2;
+
+struct alignas(16) RowP {
+    int32_t kind;  // 0 zero, 1 copy row j0, 2 lerp, 3 lerp with dx == 1 (npinterp)
+    int32_t j0;    // box-relative rows
+    int32_t j1;
+    int32_t pad;
+    double c0;  // canvas: w0 = 1-f       npinterp: t
+    double c1;  // canvas: f              npinterp: dx
+    double n0;  // canvas: -w0 * 2^52     npinterp: -t * 2^52
+    double n1;  // canvas: -f * 2^52
+};
+
+struct Params {
+    uint16_t *vol;
+    void *xy;
+    void *xz;
+    void *yz;
+    unsigned int *counters;  // [0] next item (zeroed by the host before the launch)
+    int64_t n, h, w, first, u_begin, u_count, chunk;
+    double shear;
+    int32_t UT, XT, S, n_items, xy_accumulate;
+};
+
+struct Smem {
+    uint16_t box[kStages][kBoxRows][kTX];
+    RowP rows[kStages][kTU];
+    uint32_t xz[2][kConsumerWarps][kTX];
+    uint64_t full[kStages];
+    uint64_t empty[kStages];
+    uint64_t qfull[kQueue];
+    uint64_t qempty[kQueue];
+    int32_t queue[kQueue];
+};
+
+__device__ __forceinline__ void decode(int item, const Params &p, int &ut, int &xt, int &sc) {
+    sc = item % p.S;
+    const int rest = item / p.S;
+    xt = rest % p.XT;
+    const int k = rest / p.XT;  // centre-out rank over u-tiles: heaviest tiles first
+    const int mid = (p.UT - 1) / 2;
+    const int d = (k + 1) >> 1;
+    ut = (k & 1) ? mid + d : mid - d;
+}
+
+__device__ __forceinline__ bool touches(int64_t lo, int64_t hi, int64_t tu0) {
+    return !(hi < tu0 || lo > tu0 + kTU - 1);
+}
+
+__device__ __forceinline__ double biased(uint32_t v16) { return __hiloint2double(0x43300000, (int)v16); }
+
+template <int FORMULA>
+__device__ __forceinline__ uint32_t voxel(uint32_t a, uint32_t b, const RowP &rp) {
+    if (FORMULA == SSB_FORMULA_CANVAS) {
+        const double p0 = __fma_rn(rp.c0, biased(a), rp.n0);  // == fl(w0 * a)
+        const double p1 = __fma_rn(rp.c1, biased(b), rp.n1);  // == fl(f * b)
+        return rint_to_u16(__dadd_rn(p0, p1));
+    } else {
+        const double A = __dsub_rn(biased(a), kTwo52);
+        if (rp.kind == 3) {
+            // dx == 1: slope = b - a exactly; fl(|d| * t) by the biased fma, sign restored
+            // afterwards (round-to-nearest is symmetric)
+            const int32_t d = (int32_t)b - (int32_t)a;
+            double prod = __fma_rn(rp.c0, biased((uint32_t)abs(d)), rp.n0);
+            if (d < 0) prod = -prod;
+            return rint_to_u16(__dadd_rn(prod, A));
+        }
+        const double B = __dsub_rn(biased(b), kTwo52);
+        const double slope = __ddiv_rn(__dsub_rn(B, A), rp.c1);
+        return rint_to_u16(__dadd_rn(__dmul_rn(slope, rp.c0), A));
+    }
+}
+
+template <int FORMULA>
+__device__ __forceinline__ uint4 voxels8(const uint4 a, const uint4 b, const RowP &rp) {
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+    const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t lo = voxel<FORMULA>(aw[q] & 0xFFFFu, bw[q] & 0xFFFFu, rp);
+        const uint32_t hi = voxel<FORMULA>(aw[q] >> 16, bw[q] >> 16, rp);
+        o[q] = __byte_perm(lo, hi, 0x5410);
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// Row parameters of canvas row u for one slice, box-relative (producer lanes).
+template <int INTERP, int FORMULA>
+__device__ __forceinline__ RowP make_row(int64_t u, bool in_window, int64_t lo, int64_t hi, double off,
+                                         int64_t h, int64_t box_r0) {
+    RowP o;
+    o.kind = 0;
+    o.j0 = o.j1 = 0;
+    o.pad = 0;
+    o.c0 = o.c1 = o.n0 = o.n1 = 0.0;
+    if (!in_window || u < lo || u > hi) return o;
+    const RowParam rp = row_param<INTERP, FORMULA>(u, lo, off, h);
+    o.kind = rp.kind;
+    o.j0 = (int32_t)(rp.j0 - box_r0);
+    o.j1 = (int32_t)(rp.j1 - box_r0);
+    if (rp.kind >= 2) {
+        o.c0 = rp.c0;
+        o.c1 = rp.c1;
+        o.n0 = -(rp.c0 * kTwo52);  // exact: power-of-two scaling
+        o.n1 = -(rp.c1 * kTwo52);
+    }
+    return o;
+}
+
+template <int INTERP, int FORMULA, int REDUCE>
+__global__ void __launch_bounds__(kThreads, 1)
+    deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
+    constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int k = 0; k < kStages; ++k) {
+            mbar_init(&sm.full[k], 32);
+            mbar_init(&sm.empty[k], kConsumerWarps);
+        }
+        for (int k = 0; k < kQueue; ++k) {
+            mbar_init(&sm.qfull[k], 1);
+            mbar_init(&sm.qempty[k], kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // ===================== producer warp =====================
+        if (lane == 0) prefetch_tmap(&tmap);
+        const uint64_t policy = policy_evict_first();
+        uint32_t stage = 0, sphase = 0, q = 0, qphase = 0;
+        while (true) {
+            int item = 0;
+            if (lane == 0) item = (int)atomicAdd(&p.counters[0], 1u);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            const bool done = item >= p.n_items;
+            if (lane == 0) {
+                mbar_wait(&sm.qempty[q], qphase ^ 1);
+                sm.queue[q] = done ? -1 : item;
+                mbar_arrive(&sm.qfull[q]);
+            }
+            if (++q == kQueue) { q = 0; qphase ^= 1; }
+            if (done) break;
+            int ut, xt, sc;
+            decode(item, p, ut, xt, sc);
+            const int64_t tu0 = p.u_begin + (int64_t)ut * kTU;
+            const int64_t s_begin = (int64_t)sc * p.chunk, s_end = min(p.n, s_begin + p.chunk);
+            for (int64_t s = s_begin; s < s_end; ++s) {
+                int64_t lo, hi;
+                double off;
+                slice_span(p.first + s, p.shear, p.h, INTERP, lo, hi, off);
+                if (!touches(lo, hi, tu0)) continue;
+                const int64_t base = INTERP == SSB_INTERP_NEAREST ? lo : (int64_t)floor(off);
+                const int64_t box_r0 = tu0 - base - 2;
+                if (lane == 0) mbar_wait(&sm.empty[stage], sphase ^ 1);
+                __syncwarp();
+#pragma unroll
+                for (int r = lane; r < kTU; r += 32) {
+                    const int64_t u = tu0 + r;
+                    const bool in_window = (int64_t)ut * kTU + r < p.u_count;
+                    sm.rows[stage][r] = make_row<INTERP, FORMULA>(u, in_window, lo, hi, off, p.h, box_r0);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&sm.full[stage], kBoxBytes);
+                    tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
+                                (int32_t)s, policy);
+                } else {
+                    mbar_arrive(&sm.full[stage]);
+                }
+                if (++stage == kStages) { stage = 0; sphase ^= 1; }
+            }
+        }
+        return;
+    }
+
+    // ===================== consumer warps =====================
+    uint32_t stage = 0, sphase = 0, q = 0, qphase = 0, xzb = 0;
+    const size_t frame_plane = (size_t)p.u_count * p.w;
+    while (true) {
+        int item = 0;
+        if (lane == 0) {
+            mbar_wait(&sm.qfull[q], qphase);
+            item = sm.queue[q];
+        }
+        item = __shfl_sync(0xffffffffu, item, 0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.qempty[q]);
+        if (++q == kQueue) { q = 0; qphase ^= 1; }
+        if (item < 0) break;
+
+        int ut, xt, sc;
+        decode(item, p, ut, xt, sc);
+        const int64_t tu0 = p.u_begin + (int64_t)ut * kTU;
+        const int64_t s_begin = (int64_t)sc * p.chunk, s_end = min(p.n, s_begin + p.chunk);
+        const int64_t x = (int64_t)xt * kTX + lane * 8;
+        const bool col_ok = x < p.w;
+        const int64_t r0 = (int64_t)ut * kTU + warp * kRows;  // row (within the window) of k = 0
+
+        uint4 acc_max[kRows];
+        uint32_t acc_sum[kMax ? 1 : kRows][8];
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) {
+            acc_max[k] = make_uint4(0, 0, 0, 0);
+            if (!kMax)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc_sum[k][c] = 0;
+        }
+
+        for (int64_t s = s_begin; s < s_end; ++s) {
+            int64_t lo, hi;
+            double off;
+            slice_span(p.first + s, p.shear, p.h, INTERP, lo, hi, off);
+            const bool hit = touches(lo, hi, tu0);
+            if (hit) mbar_wait(&sm.full[stage], sphase);
+            uint4 xz_max = make_uint4(0, 0, 0, 0);
+            uint32_t xz_sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int k = 0; k < kRows; ++k) {
+                const int64_t r = r0 + k;
+                const bool row_ok = r < p.u_count;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (hit) {
+                    const RowP &rp = sm.rows[stage][warp * kRows + k];
+                    if (rp.kind != 0) {
+                        const uint4 a = *reinterpret_cast<const uint4 *>(&sm.box[stage][rp.j0][lane * 8]);
+                        if (rp.kind == 1) {
+                            v = a;
+                        } else {
+                            const uint4 b = *reinterpret_cast<const uint4 *>(&sm.box[stage][rp.j1][lane * 8]);
+                            v = voxels8<FORMULA>(a, b, rp);
+                        }
+                    }
+                }
+                if (p.vol != nullptr && row_ok && col_ok)
+                    stg_cs_v4(p.vol + (size_t)s * frame_plane + (size_t)r * p.w + x, v);
+                if (kMax) {
+                    acc_max[k] = max_u16x8(acc_max[k], v);
+                    xz_max = max_u16x8(xz_max, v);
+                } else {
+                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint32_t e = (w4[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                        acc_sum[k][c] += e;
+                        xz_sum[c] += e;
+                    }
+                }
+                if (p.yz != nullptr) {
+                    const uint32_t part = kMax ? hmax_u16x8(v) : hsum_u16x8(v);
+                    const uint32_t red = kMax ? __reduce_max_sync(0xffffffffu, part)
+                                              : __reduce_add_sync(0xffffffffu, part);
+                    if (lane == 0 && row_ok) {
+                        const size_t idx = ((size_t)xt * p.n + s) * p.u_count + r;
+                        if (kMax) static_cast<uint16_t *>(p.yz)[idx] = (uint16_t)red;
+                        else static_cast<uint32_t *>(p.yz)[idx] = red;
+                    }
+                }
+            }
+            if (hit) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[stage]);
+                if (++stage == kStages) { stage = 0; sphase ^= 1; }
+            }
+            if (p.xz != nullptr) {
+                uint32_t *dst = &sm.xz[xzb][warp][lane * 8];
+                if (kMax) {
+                    const uint32_t w4[4] = {xz_max.x, xz_max.y, xz_max.z, xz_max.w};
+                    *reinterpret_cast<uint4 *>(dst) =
+                        make_uint4(w4[0] & 0xFFFFu, w4[0] >> 16, w4[1] & 0xFFFFu, w4[1] >> 16);
+                    *reinterpret_cast<uint4 *>(dst + 4) =
+                        make_uint4(w4[2] & 0xFFFFu, w4[2] >> 16, w4[3] & 0xFFFFu, w4[3] >> 16);
+                } else {
+                    *reinterpret_cast<uint4 *>(dst) = make_uint4(xz_sum[0], xz_sum[1], xz_sum[2], xz_sum[3]);
+                    *reinterpret_cast<uint4 *>(dst + 4) = make_uint4(xz_sum[4], xz_sum[5], xz_sum[6], xz_sum[7]);
+                }
+                named_bar_sync(1, kConsumerThreads);
+                if (tid < kTX) {
+                    const int64_t col = (int64_t)xt * kTX + tid;
+                    if (col < p.w) {
+                        uint32_t red = 0;
+#pragma unroll
+                        for (int w2 = 0; w2 < kConsumerWarps; ++w2)
+                            red = kMax ? max(red, sm.xz[xzb][w2][tid]) : red + sm.xz[xzb][w2][tid];
+                        const size_t idx = ((size_t)ut * p.n + s) * p.w + col;
+                        if (kMax) static_cast<uint16_t *>(p.xz)[idx] = (uint16_t)red;
+                        else static_cast<uint32_t *>(p.xz)[idx] = red;
+                    }
+                }
+                xzb ^= 1;
+            }
+        }
+
+        if (p.xy != nullptr && col_ok) {
+#pragma unroll
+            for (int k = 0; k < kRows; ++k) {
+                const int64_t r = r0 + k;
+                if (r >= p.u_count) break;
+                const size_t base = (size_t)sc * frame_plane + (size_t)r * p.w + x;
+                if (kMax) {
+                    uint16_t *dst = static_cast<uint16_t *>(p.xy) + base;
+                    uint4 v = acc_max[k];
+                    if (p.xy_accumulate) v = max_u16x8(v, *reinterpret_cast<const uint4 *>(dst));
+                    *reinterpret_cast<uint4 *>(dst) = v;
+                } else {
+                    uint32_t *dst = static_cast<uint32_t *>(p.xy) + base;
+                    uint4 v0 = make_uint4(acc_sum[k][0], acc_sum[k][1], acc_sum[k][2], acc_sum[k][3]);
+                    uint4 v1 = make_uint4(acc_sum[k][4], acc_sum[k][5], acc_sum[k][6], acc_sum[k][7]);
+                    if (p.xy_accumulate) {
+                        const uint4 o0 = *reinterpret_cast<const uint4 *>(dst);
+                        const uint4 o1 = *reinterpret_cast<const uint4 *>(dst + 4);
+                        v0 = make_uint4(v0.x + o0.x, v0.y + o0.y, v0.z + o0.z, v0.w + o0.w);
+                        v1 = make_uint4(v1.x + o1.x, v1.y + o1.y, v1.z + o1.z, v1.w + o1.w);
+                    }
+                    *reinterpret_cast<uint4 *>(dst) = v0;
+                    *reinterpret_cast<uint4 *>(dst + 4) = v1;
+                }
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------------------- host
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void *ptr = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &ptr, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+template <int INTERP, int FORMULA, int REDUCE>
+int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
+    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    kern<<<grid, kThreads, sizeof(Smem), st>>>(map, prm);
+    return check_launch("deskew_tma_kernel");
+}
+
+}  // namespace tma_path
+
+bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol, const void *xy) {
+    if (d.width % 8 != 0 || !aligned16(raw) || !aligned16(vol) || !aligned16(xy)) return false;
+    if (d.n > INT32_MAX || d.height > INT32_MAX || d.width > INT32_MAX) return false;
+    return tma_path::encode_fn() != nullptr;
+}
+
+int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz,
+                      void *yz, unsigned int *counters, int64_t UT, int64_t XT, int64_t S, int64_t chunk,
+                      int xy_accumulate, cudaStream_t st) {
+    using namespace tma_path;
+    CUtensorMap map;
+    const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)d.n};
+    const cuuint64_t strides[2] = {(cuuint64_t)d.width * 2, (cuuint64_t)d.width * d.height * 2};
+    const cuuint32_t box[3] = {(cuuint32_t)kTX, (cuuint32_t)kBoxRows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t *>(raw), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SSB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    const int64_t items = UT * XT * S;
+    if (items > INT32_MAX / 2) return fail(SSB_ERR_CAPACITY, "too many tiles");
+
+    Params prm{};
+    prm.vol = vol;
+    prm.xy = xy;
+    prm.xz = xz;
+    prm.yz = yz;
+    prm.counters = counters;
+    prm.n = d.n;
+    prm.h = d.height;
+    prm.w = d.width;
+    prm.first = d.first_slice;
+    prm.u_begin = d.u_begin;
+    prm.u_count = d.u_count;
+    prm.chunk = chunk;
+    prm.shear = d.shear_px;
+    prm.UT = (int32_t)UT;
+    prm.XT = (int32_t)XT;
+    prm.S = (int32_t)S;
+    prm.n_items = (int32_t)items;
+    prm.xy_accumulate = xy_accumulate;
+    const int grid = (int)std::min<int64_t>(items, num_sms());
+    if (cudaMemsetAsync(counters, 0, sizeof(unsigned int), st) != cudaSuccess)
+        return fail(SSB_ERR_CUDA, "scheduler counter reset failed");
+
+    int rc;
+    const bool mx = d.reduce == SSB_REDUCE_MAX;
+    if (d.interp == SSB_INTERP_NEAREST)
+        rc = mx ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX>(map, prm, grid, st)
+                : launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM>(map, prm, grid, st);
+    else if (d.formula == SSB_FORMULA_CANVAS)
+        rc = mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX>(map, prm, grid, st)
+                : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM>(map, prm, grid, st);
+    else
+        rc = mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_MAX>(map, prm, grid, st)
+                : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM>(map, prm, grid, st);
+    count_launches(1);
+    return rc;
+}
+
+}  // namespace ssb

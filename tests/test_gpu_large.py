@@ -23,9 +23,18 @@ def synthetic(n, h, w, seed, hi=4096):
     return torch.randint(0, hi, (n, h, w), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
 
 
+@pytest.fixture(params=["tma", "tiled"])
+def kernel_path(request, monkeypatch):
+    if request.param == "tiled":
+        monkeypatch.setenv("SSB_DISABLE_TMA", "1")
+    else:
+        monkeypatch.delenv("SSB_DISABLE_TMA", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("interp", ["linear", "nearest"])
 @pytest.mark.parametrize("reduce", ["max", "sum"])
-def test_config1_full_parity(interp, reduce):
+def test_config1_full_parity(interp, reduce, kernel_path):
     raw = synthetic(128, 256, 512, 1, hi=65536)
     res = deskew_device(raw, S30, interp, reduce=reduce)
     torch.cuda.synchronize()
@@ -54,7 +63,7 @@ def _reduce_dev(vol: torch.Tensor, axis: int, reduce: str) -> np.ndarray:
 
 
 @pytest.mark.parametrize("reduce", ["max", "sum"])
-def test_config2_properties(reduce):
+def test_config2_properties(reduce, kernel_path):
     n, h, w = 512, 2048, 2048
     raw = synthetic(n, h, w, 2)
     res = deskew_device(raw, S30, "linear", reduce=reduce)

@@ -39,9 +39,19 @@ def frame(arr, i, **kw):
 # golden fixtures produced by the reference itself
 
 
+@pytest.fixture(params=["tma", "tiled"])
+def kernel_path(request, monkeypatch):
+    """Run a test through the TMA persistent kernel and through the tiled fallback."""
+    if request.param == "tiled":
+        monkeypatch.setenv("SSB_DISABLE_TMA", "1")
+    else:
+        monkeypatch.delenv("SSB_DISABLE_TMA", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
 @pytest.mark.parametrize("reduce", ["max", "sum"])
-def test_fused_kernel_matches_reference_fixtures(case, reduce):
+def test_fused_kernel_matches_reference_fixtures(case, reduce, kernel_path):
     st, s, interp = case["stack"], float(case["shear"]), str(case["interp"])
     for formula, key in (("canvas", "vol"), ("npinterp", "batch_vol")):
         vol, pr = run(st, s, interp, formula, reduce)
@@ -301,7 +311,7 @@ class TestReferenceDeskew:
 
 
 @pytest.mark.parametrize("seed", range(12))
-def test_random_shapes_vs_oracle(seed):
+def test_random_shapes_vs_oracle(seed, kernel_path):
     rng = np.random.default_rng(1000 + seed)
     n, h, w = int(rng.integers(1, 40)), int(rng.integers(1, 90)), int(rng.integers(1, 600))
     s = float(rng.choice([rng.uniform(0, 3), 0.8660254037844386, 0.7071067811865476, 1.0, 0.5, 0.0]))
@@ -331,7 +341,7 @@ def test_unaligned_and_ragged_buffers():
         np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
 
 
-def test_slab_window_uses_global_indices():
+def test_slab_window_uses_global_indices(kernel_path):
     rng = np.random.default_rng(9)
     st = rng.integers(0, 65536, (60, 50, 264)).astype(np.uint16)
     s = 0.7071067811865476
@@ -347,7 +357,7 @@ def test_slab_window_uses_global_indices():
     np.testing.assert_array_equal(pr[2], full[2][20:45, lo:hi + 1])
 
 
-def test_streamer_chunks_match_single_launch():
+def test_streamer_chunks_match_single_launch(kernel_path):
     from paper_2211_00645_b200.stream import StackStreamer, pinned_stack
     rng = np.random.default_rng(4)
     n, h, w, s = 37, 48, 256, 0.8660254037844386

@@ -1,0 +1,36 @@
+"""Small driver for ncu captures: config-2 fused deskew launches, nothing else."""
+import argparse
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2211_00645_b200.deskew import deskew_device  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--interp", default="linear")
+ap.add_argument("--reduce", default="max")
+ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--n", type=int, default=512)
+ap.add_argument("--hw", type=int, default=2048)
+ap.add_argument("--no-volume", action="store_true")
+ap.add_argument("--formula", default="canvas")
+a = ap.parse_args()
+s = math.cos(math.radians(30.0))
+g = torch.Generator(device="cuda").manual_seed(1234)
+raw = torch.randint(0, 4096, (a.n, a.hw, a.hw), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
+res = None
+for _ in range(a.iters):
+    res = deskew_device(raw, s, a.interp, reduce=a.reduce, formula=a.formula, write_volume=not a.no_volume)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(a.iters):
+    deskew_device(raw, s, a.interp, reduce=a.reduce, formula=a.formula, write_volume=not a.no_volume,
+                  volume=res.volume, projections=res.projections)
+e1.record()
+torch.cuda.synchronize()
+print(f"{a.interp} {a.reduce} vol={not a.no_volume}: {e0.elapsed_time(e1) / a.iters:.3f} ms/call")
