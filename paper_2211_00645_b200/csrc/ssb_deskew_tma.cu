@@ -33,25 +33,30 @@ namespace ssb {
 namespace tma_path {
 
 constexpr int kConsumerWarps = 15;  // + 1 producer = 16 warps: 128 registers per thread
-constexpr int kRows = 4;  // canvas rows per consumer warp
+constexpr int kRows = 4;            // canvas rows per consumer warp
 constexpr int kTU = kConsumerWarps * kRows;
-constexpr int kBoxRows = kTU + 4;  // +2 rows of slack on each side of the tile
+constexpr int kBoxRows = kTU + 4;  // 2 rows of slack on each side of the tile
 constexpr int kTX = 256;
-constexpr int kStages = 4;
+constexpr int kStages = 5;
 constexpr int kQueue = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr uint32_t kBoxBytes = kBoxRows * kTX * 2;
+constexpr uint32_t kRowBytes = kTX * 2;
+constexpr int kXzWords = 2 * 2 * kConsumerWarps * (kTX / 2);  // 2 buffers x 2 slices x warps x u16x2
 
+// Sampling parameters of one canvas row for one slice (written by the producer).
+// Rows outside the slice's span point both taps at a shared zero row with weights
+// (1, 0), which yields exactly 0 -- the consumer loop has no per-row branches.
 struct alignas(16) RowP {
-    int32_t kind;  // 0 zero, 1 copy row j0, 2 lerp, 3 lerp with dx == 1 (npinterp)
-    int32_t j0;    // box-relative rows
-    int32_t j1;
+    double c0;       // canvas: w0 = 1-f       npinterp: t
+    double c1;       // canvas: f              npinterp: dx
+    double n0;       // -c0 * 2^52
+    double n1;       // -c1 * 2^52
+    uint32_t off_a;  // shared-memory byte address of tap a (row j0)
+    uint32_t off_b;  // tap b (row j1)
+    int32_t kind;    // npinterp only: 3 = dx == 1 (incl. copies, t = 0), 2 = general dx
     int32_t pad;
-    double c0;  // canvas: w0 = 1-f       npinterp: t
-    double c1;  // canvas: f              npinterp: dx
-    double n0;  // canvas: -w0 * 2^52     npinterp: -t * 2^52
-    double n1;  // canvas: -f * 2^52
 };
 
 struct Params {
@@ -67,8 +72,10 @@ struct Params {
 
 struct Smem {
     uint16_t box[kStages][kBoxRows][kTX];
+    uint16_t zero_row[kTX];
     RowP rows[kStages][kTU];
-    uint32_t xz[2][kConsumerWarps][kTX];
+    uint32_t hdr[kStages];  // bit 16: slice touches the tile (box loaded); bits 0..14: warps with live rows
+    alignas(16) uint32_t xz[kXzWords];
     uint64_t full[kStages];
     uint64_t empty[kStages];
     uint64_t qfull[kQueue];
@@ -86,75 +93,96 @@ __device__ __forceinline__ void decode(int item, const Params &p, int &ut, int &
     ut = (k & 1) ? mid + d : mid - d;
 }
 
-__device__ __forceinline__ bool touches(int64_t lo, int64_t hi, int64_t tu0) {
-    return !(hi < tu0 || lo > tu0 + kTU - 1);
-}
-
 __device__ __forceinline__ double biased(uint32_t v16) { return __hiloint2double(0x43300000, (int)v16); }
 
 template <int FORMULA>
-__device__ __forceinline__ uint32_t voxel(uint32_t a, uint32_t b, const RowP &rp) {
+__device__ __forceinline__ uint32_t voxel(uint32_t a, uint32_t b, const double c0, const double c1,
+                                          const double n0, const double n1, const int kind) {
     if (FORMULA == SSB_FORMULA_CANVAS) {
-        const double p0 = __fma_rn(rp.c0, biased(a), rp.n0);  // == fl(w0 * a)
-        const double p1 = __fma_rn(rp.c1, biased(b), rp.n1);  // == fl(f * b)
-        return rint_to_u16(__dadd_rn(p0, p1));
+        const double p0 = __fma_rn(c0, biased(a), n0);  // == fl(w0 * a)
+        const double p1 = __fma_rn(c1, biased(b), n1);  // == fl(f * b)
+        return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(p0, p1), kRintMagic));
     } else {
         const double A = __dsub_rn(biased(a), kTwo52);
-        if (rp.kind == 3) {
+        if (kind == 3) {
             // dx == 1: slope = b - a exactly; fl(|d| * t) by the biased fma, sign restored
             // afterwards (round-to-nearest is symmetric)
             const int32_t d = (int32_t)b - (int32_t)a;
-            double prod = __fma_rn(rp.c0, biased((uint32_t)abs(d)), rp.n0);
+            double prod = __fma_rn(c0, biased((uint32_t)abs(d)), n0);
             if (d < 0) prod = -prod;
-            return rint_to_u16(__dadd_rn(prod, A));
+            return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(prod, A), kRintMagic));
         }
         const double B = __dsub_rn(biased(b), kTwo52);
-        const double slope = __ddiv_rn(__dsub_rn(B, A), rp.c1);
-        return rint_to_u16(__dadd_rn(__dmul_rn(slope, rp.c0), A));
+        const double slope = __ddiv_rn(__dsub_rn(B, A), c1);
+        return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(__dmul_rn(slope, c0), A), kRintMagic));
     }
 }
 
 template <int FORMULA>
 __device__ __forceinline__ uint4 voxels8(const uint4 a, const uint4 b, const RowP &rp) {
+    const double c0 = rp.c0, c1 = rp.c1, n0 = rp.n0, n1 = rp.n1;
+    const int kind = FORMULA == SSB_FORMULA_CANVAS ? 2 : rp.kind;
     const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
     const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
     uint32_t o[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const uint32_t lo = voxel<FORMULA>(aw[q] & 0xFFFFu, bw[q] & 0xFFFFu, rp);
-        const uint32_t hi = voxel<FORMULA>(aw[q] >> 16, bw[q] >> 16, rp);
+        const uint32_t lo = voxel<FORMULA>(aw[q] & 0xFFFFu, bw[q] & 0xFFFFu, c0, c1, n0, n1, kind);
+        const uint32_t hi = voxel<FORMULA>(aw[q] >> 16, bw[q] >> 16, c0, c1, n0, n1, kind);
         o[q] = __byte_perm(lo, hi, 0x5410);
     }
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-// Row parameters of canvas row u for one slice, box-relative (producer lanes).
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t hmax8(const uint4 v) {
+    const uint32_t m = __vmaxu2(__vmaxu2(__vmaxu2(v.x, v.y), v.z), v.w);  // ptxas fuses into VIMNMX3
+    return max(m & 0xFFFFu, m >> 16);
+}
+
+// Row table entry of canvas row u for one slice (producer lanes).  Returns whether
+// the row is live (inside the window and the slice's span).
 template <int INTERP, int FORMULA>
-__device__ __forceinline__ RowP make_row(int64_t u, bool in_window, int64_t lo, int64_t hi, double off,
-                                         int64_t h, int64_t box_r0) {
-    RowP o;
-    o.kind = 0;
-    o.j0 = o.j1 = 0;
+__device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int64_t lo, int64_t hi, double off,
+                                         int64_t h, int64_t box_r0, uint32_t box_addr, uint32_t zero_addr) {
+    o.c0 = 1.0;
+    o.c1 = 0.0;
+    o.n0 = -kTwo52;
+    o.n1 = -0.0;
+    o.off_a = o.off_b = zero_addr;
+    o.kind = 3;
     o.pad = 0;
-    o.c0 = o.c1 = o.n0 = o.n1 = 0.0;
-    if (!in_window || u < lo || u > hi) return o;
+    if (FORMULA == SSB_FORMULA_NPINTERP) {
+        o.c0 = 0.0;  // t = 0: copy of tap a (the zero row)
+        o.n0 = -0.0;
+    }
+    if (!in_window || u < lo || u > hi) return false;
     const RowParam rp = row_param<INTERP, FORMULA>(u, lo, off, h);
-    o.kind = rp.kind;
-    o.j0 = (int32_t)(rp.j0 - box_r0);
-    o.j1 = (int32_t)(rp.j1 - box_r0);
+    o.off_a = box_addr + (uint32_t)(rp.j0 - box_r0) * kRowBytes;
+    o.off_b = box_addr + (uint32_t)(rp.j1 - box_r0) * kRowBytes;
     if (rp.kind >= 2) {
         o.c0 = rp.c0;
         o.c1 = rp.c1;
         o.n0 = -(rp.c0 * kTwo52);  // exact: power-of-two scaling
         o.n1 = -(rp.c1 * kTwo52);
+        o.kind = rp.kind;
+    } else if (FORMULA == SSB_FORMULA_CANVAS) {
+        // copy (only reachable for h == 1 paths): w0 = 1, f = 0
+        o.off_b = o.off_a;
     }
-    return o;
+    return true;
 }
 
 template <int INTERP, int FORMULA, int REDUCE>
 __global__ void __launch_bounds__(kThreads, 1)
     deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
+    constexpr int kXzBatch = kMax ? 2 : 1;  // slices per XZ reduction (smem budget)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -170,12 +198,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_mbar_init();
     }
+    for (int k = tid; k < kTX; k += kThreads) sm.zero_row[k] = 0;
     __syncthreads();
 
     if (warp == kConsumerWarps) {
         // ===================== producer warp =====================
         if (lane == 0) prefetch_tmap(&tmap);
         const uint64_t policy = policy_evict_first();
+        const uint32_t zero_addr = smem_addr(sm.zero_row);
         uint32_t stage = 0, sphase = 0, q = 0, qphase = 0;
         while (true) {
             int item = 0;
@@ -197,22 +227,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int64_t lo, hi;
                 double off;
                 slice_span(p.first + s, p.shear, p.h, INTERP, lo, hi, off);
-                if (!touches(lo, hi, tu0)) continue;
+                const bool hit = !(hi < tu0 || lo > tu0 + kTU - 1);
                 const int64_t base = INTERP == SSB_INTERP_NEAREST ? lo : (int64_t)floor(off);
                 const int64_t box_r0 = tu0 - base - 2;
                 if (lane == 0) mbar_wait(&sm.empty[stage], sphase ^ 1);
                 __syncwarp();
+                uint32_t live_lo = 0, live_hi = 0;
+                if (hit) {
+                    const uint32_t box_addr = smem_addr(&sm.box[stage][0][0]);
+                    bool l0, l1 = false;
+                    {
+                        const int r = lane;
+                        l0 = make_row<INTERP, FORMULA>(sm.rows[stage][r], tu0 + r, (int64_t)ut * kTU + r < p.u_count,
+                                                       lo, hi, off, p.h, box_r0, box_addr, zero_addr);
+                    }
+                    if (lane + 32 < kTU) {
+                        const int r = lane + 32;
+                        l1 = make_row<INTERP, FORMULA>(sm.rows[stage][r], tu0 + r, (int64_t)ut * kTU + r < p.u_count,
+                                                       lo, hi, off, p.h, box_r0, box_addr, zero_addr);
+                    }
+                    live_lo = __ballot_sync(0xffffffffu, l0);
+                    live_hi = __ballot_sync(0xffffffffu, l1);
+                }
+                if (lane == 0) {
+                    const uint64_t live = (uint64_t)live_lo | ((uint64_t)live_hi << 32);
+                    uint32_t mask = 0;
 #pragma unroll
-                for (int r = lane; r < kTU; r += 32) {
-                    const int64_t u = tu0 + r;
-                    const bool in_window = (int64_t)ut * kTU + r < p.u_count;
-                    sm.rows[stage][r] = make_row<INTERP, FORMULA>(u, in_window, lo, hi, off, p.h, box_r0);
+                    for (int w = 0; w < kConsumerWarps; ++w)
+                        if ((live >> (w * kRows)) & ((1u << kRows) - 1)) mask |= 1u << w;
+                    sm.hdr[stage] = mask | (hit ? (1u << 16) : 0u);
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&sm.full[stage], kBoxBytes);
-                    tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
-                                (int32_t)s, policy);
+                    if (hit) {
+                        mbar_arrive_expect_tx(&sm.full[stage], kBoxBytes);
+                        tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
+                                    (int32_t)s, policy);
+                    } else {
+                        mbar_arrive(&sm.full[stage]);
+                    }
                 } else {
                     mbar_arrive(&sm.full[stage]);
                 }
@@ -223,8 +276,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ===================== consumer warps =====================
-    uint32_t stage = 0, sphase = 0, q = 0, qphase = 0, xzb = 0;
-    const size_t frame_plane = (size_t)p.u_count * p.w;
+    uint32_t stage = 0, sphase = 0, q = 0, qphase = 0, xz_batch = 0;
+    const size_t plane = (size_t)p.u_count * p.w;
+    const uint32_t lane_off = lane * 16;
     while (true) {
         int item = 0;
         if (lane == 0) {
@@ -239,11 +293,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         int ut, xt, sc;
         decode(item, p, ut, xt, sc);
-        const int64_t tu0 = p.u_begin + (int64_t)ut * kTU;
         const int64_t s_begin = (int64_t)sc * p.chunk, s_end = min(p.n, s_begin + p.chunk);
         const int64_t x = (int64_t)xt * kTX + lane * 8;
         const bool col_ok = x < p.w;
-        const int64_t r0 = (int64_t)ut * kTU + warp * kRows;  // row (within the window) of k = 0
+        const int64_t r0 = (int64_t)ut * kTU + warp * kRows;  // window row of k = 0
+        const int64_t rows_left = p.u_count - r0;
+        const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= kRows ? kRows : (int)rows_left);
+        uint16_t *vrow = p.vol != nullptr ? p.vol + (size_t)s_begin * plane + (size_t)r0 * p.w + x : nullptr;
+        const size_t yz_base = ((size_t)xt * p.n + s_begin) * p.u_count + r0;
 
         uint4 acc_max[kRows];
         uint32_t acc_sum[kMax ? 1 : kRows][8];
@@ -256,102 +313,113 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         for (int64_t s = s_begin; s < s_end; ++s) {
-            int64_t lo, hi;
-            double off;
-            slice_span(p.first + s, p.shear, p.h, INTERP, lo, hi, off);
-            const bool hit = touches(lo, hi, tu0);
-            if (hit) mbar_wait(&sm.full[stage], sphase);
+            mbar_wait(&sm.full[stage], sphase);
+            const uint32_t hdr = sm.hdr[stage];
+            const bool live = (hdr >> 16) & (hdr >> warp) & 1u;
             uint4 xz_max = make_uint4(0, 0, 0, 0);
             uint32_t xz_sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            uint32_t yzv[kRows] = {0, 0, 0, 0};
+            if (live) {
 #pragma unroll
-            for (int k = 0; k < kRows; ++k) {
-                const int64_t r = r0 + k;
-                const bool row_ok = r < p.u_count;
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (hit) {
+                for (int k = 0; k < kRows; ++k) {
                     const RowP &rp = sm.rows[stage][warp * kRows + k];
-                    if (rp.kind != 0) {
-                        const uint4 a = *reinterpret_cast<const uint4 *>(&sm.box[stage][rp.j0][lane * 8]);
-                        if (rp.kind == 1) {
-                            v = a;
-                        } else {
-                            const uint4 b = *reinterpret_cast<const uint4 *>(&sm.box[stage][rp.j1][lane * 8]);
-                            v = voxels8<FORMULA>(a, b, rp);
-                        }
+                    const uint4 a = lds128(rp.off_a + lane_off);
+                    uint4 v;
+                    if (INTERP == SSB_INTERP_NEAREST) {
+                        v = a;
+                    } else {
+                        const uint4 b = lds128(rp.off_b + lane_off);
+                        v = voxels8<FORMULA>(a, b, rp);
                     }
-                }
-                if (p.vol != nullptr && row_ok && col_ok)
-                    stg_cs_v4(p.vol + (size_t)s * frame_plane + (size_t)r * p.w + x, v);
-                if (kMax) {
-                    acc_max[k] = max_u16x8(acc_max[k], v);
-                    xz_max = max_u16x8(xz_max, v);
-                } else {
-                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                    if (vrow != nullptr && k < rows_ok && col_ok) stg_cs_v4(vrow + (size_t)k * p.w, v);
+                    if (kMax) {
+                        acc_max[k] = max_u16x8(acc_max[k], v);
+                        xz_max = max_u16x8(xz_max, v);
+                        if (p.yz != nullptr) yzv[k] = __reduce_max_sync(0xffffffffu, hmax8(v));
+                    } else {
+                        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                        uint32_t rs = 0;
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint32_t e = (w4[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
-                        acc_sum[k][c] += e;
-                        xz_sum[c] += e;
+                        for (int c = 0; c < 8; ++c) {
+                            const uint32_t e = (w4[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                            acc_sum[k][c] += e;
+                            xz_sum[c] += e;
+                            rs += e;
+                        }
+                        if (p.yz != nullptr) yzv[k] = __reduce_add_sync(0xffffffffu, rs);
                     }
                 }
-                if (p.yz != nullptr) {
-                    const uint32_t part = kMax ? hmax_u16x8(v) : hsum_u16x8(v);
-                    const uint32_t red = kMax ? __reduce_max_sync(0xffffffffu, part)
-                                              : __reduce_add_sync(0xffffffffu, part);
-                    if (lane == 0 && row_ok) {
-                        const size_t idx = ((size_t)xt * p.n + s) * p.u_count + r;
-                        if (kMax) static_cast<uint16_t *>(p.yz)[idx] = (uint16_t)red;
-                        else static_cast<uint32_t *>(p.yz)[idx] = red;
-                    }
-                }
+            } else if (vrow != nullptr && col_ok) {
+                const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int k = 0; k < kRows; ++k)
+                    if (k < rows_ok) stg_cs_v4(vrow + (size_t)k * p.w, z);
             }
-            if (hit) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[stage]);
-                if (++stage == kStages) { stage = 0; sphase ^= 1; }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[stage]);
+            if (++stage == kStages) { stage = 0; sphase ^= 1; }
+            if (vrow != nullptr) vrow += plane;
+
+            if (p.yz != nullptr && lane < rows_ok) {
+                const uint32_t val = lane == 0 ? yzv[0] : lane == 1 ? yzv[1] : lane == 2 ? yzv[2] : yzv[3];
+                const size_t idx = yz_base + (size_t)(s - s_begin) * p.u_count + lane;
+                if (kMax) static_cast<uint16_t *>(p.yz)[idx] = (uint16_t)val;
+                else static_cast<uint32_t *>(p.yz)[idx] = val;
             }
+
             if (p.xz != nullptr) {
-                uint32_t *dst = &sm.xz[xzb][warp][lane * 8];
+                const int g = (int)((s - s_begin) % kXzBatch);
+                const int buf = xz_batch & 1;
                 if (kMax) {
-                    const uint32_t w4[4] = {xz_max.x, xz_max.y, xz_max.z, xz_max.w};
-                    *reinterpret_cast<uint4 *>(dst) =
-                        make_uint4(w4[0] & 0xFFFFu, w4[0] >> 16, w4[1] & 0xFFFFu, w4[1] >> 16);
-                    *reinterpret_cast<uint4 *>(dst + 4) =
-                        make_uint4(w4[2] & 0xFFFFu, w4[2] >> 16, w4[3] & 0xFFFFu, w4[3] >> 16);
+                    uint32_t *dst = &sm.xz[((buf * 2 + g) * kConsumerWarps + warp) * (kTX / 2) + lane * 4];
+                    *reinterpret_cast<uint4 *>(dst) = xz_max;
                 } else {
+                    uint32_t *dst = &sm.xz[(buf * kConsumerWarps + warp) * kTX + lane * 8];
                     *reinterpret_cast<uint4 *>(dst) = make_uint4(xz_sum[0], xz_sum[1], xz_sum[2], xz_sum[3]);
                     *reinterpret_cast<uint4 *>(dst + 4) = make_uint4(xz_sum[4], xz_sum[5], xz_sum[6], xz_sum[7]);
                 }
-                named_bar_sync(1, kConsumerThreads);
-                if (tid < kTX) {
-                    const int64_t col = (int64_t)xt * kTX + tid;
-                    if (col < p.w) {
-                        uint32_t red = 0;
+                const bool flush = g == kXzBatch - 1 || s + 1 == s_end;
+                if (flush) {
+                    named_bar_sync(1, kConsumerThreads);
+                    const int64_t s0 = s - g;  // first slice of this batch
+                    if (kMax) {
+                        // thread -> (slice of batch, word of 2 columns)
+                        const int gg = tid / (kTX / 2), c2 = tid % (kTX / 2);
+                        const int64_t col = (int64_t)xt * kTX + 2 * c2;
+                        if (gg <= g && col < p.w) {
+                            uint32_t red = 0;
 #pragma unroll
-                        for (int w2 = 0; w2 < kConsumerWarps; ++w2)
-                            red = kMax ? max(red, sm.xz[xzb][w2][tid]) : red + sm.xz[xzb][w2][tid];
-                        const size_t idx = ((size_t)ut * p.n + s) * p.w + col;
-                        if (kMax) static_cast<uint16_t *>(p.xz)[idx] = (uint16_t)red;
-                        else static_cast<uint32_t *>(p.xz)[idx] = red;
+                            for (int w2 = 0; w2 < kConsumerWarps; ++w2)
+                                red = __vmaxu2(red, sm.xz[((buf * 2 + gg) * kConsumerWarps + w2) * (kTX / 2) + c2]);
+                            uint16_t *dst = static_cast<uint16_t *>(p.xz) + ((size_t)ut * p.n + s0 + gg) * p.w + col;
+                            *reinterpret_cast<uint32_t *>(dst) = red;
+                        }
+                    } else if (tid < kTX) {
+                        const int64_t col = (int64_t)xt * kTX + tid;
+                        if (col < p.w) {
+                            uint32_t red = 0;
+#pragma unroll
+                            for (int w2 = 0; w2 < kConsumerWarps; ++w2) red += sm.xz[(buf * kConsumerWarps + w2) * kTX + tid];
+                            static_cast<uint32_t *>(p.xz)[((size_t)ut * p.n + s0) * p.w + col] = red;
+                        }
                     }
+                    ++xz_batch;
                 }
-                xzb ^= 1;
             }
         }
 
         if (p.xy != nullptr && col_ok) {
+            const size_t base = (size_t)sc * plane + (size_t)r0 * p.w + x;
 #pragma unroll
             for (int k = 0; k < kRows; ++k) {
-                const int64_t r = r0 + k;
-                if (r >= p.u_count) break;
-                const size_t base = (size_t)sc * frame_plane + (size_t)r * p.w + x;
+                if (k >= rows_ok) break;
                 if (kMax) {
-                    uint16_t *dst = static_cast<uint16_t *>(p.xy) + base;
+                    uint16_t *dst = static_cast<uint16_t *>(p.xy) + base + (size_t)k * p.w;
                     uint4 v = acc_max[k];
                     if (p.xy_accumulate) v = max_u16x8(v, *reinterpret_cast<const uint4 *>(dst));
                     *reinterpret_cast<uint4 *>(dst) = v;
                 } else {
-                    uint32_t *dst = static_cast<uint32_t *>(p.xy) + base;
+                    uint32_t *dst = static_cast<uint32_t *>(p.xy) + base + (size_t)k * p.w;
                     uint4 v0 = make_uint4(acc_sum[k][0], acc_sum[k][1], acc_sum[k][2], acc_sum[k][3]);
                     uint4 v1 = make_uint4(acc_sum[k][4], acc_sum[k][5], acc_sum[k][6], acc_sum[k][7]);
                     if (p.xy_accumulate) {
