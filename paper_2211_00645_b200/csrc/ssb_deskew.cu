@@ -330,9 +330,8 @@ using namespace ssb;
 
 extern "C" size_t ssb_deskew_workspace_bytes(const ssb_deskew_desc *d) {
     if (validate(d) != SSB_OK) return 0;
-    const Plan a = make_plan(*d, true, true, true, kTmaTileRows, true);
     const Plan b = make_plan(*d, true, true, true, tiled_rows(*d), false);
-    return kCounterBytes + std::max(a.xy_ws + a.xz_ws + a.yz_ws, b.xy_ws + b.xz_ws + b.yz_ws);
+    return std::max(tma_workspace_bytes(*d), kCounterBytes + b.xy_ws + b.xz_ws + b.yz_ws);
 }
 
 extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_t *vol, void *xy,
@@ -348,27 +347,19 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
     }
     if (raw == nullptr) return fail(SSB_ERR_PARAM, "raw frames pointer is null");
     const bool use_tma = env_int("SSB_DISABLE_TMA", 0) == 0 && tma_eligible(*d, raw, vol, xy);
-    const Plan pl = make_plan(*d, xy != nullptr, xz != nullptr, yz != nullptr,
-                              use_tma ? kTmaTileRows : tiled_rows(*d), use_tma);
+    if (use_tma) return launch_deskew_tma(*d, raw, vol, xy, xz, yz, workspace, workspace_bytes, st);
+
+    const Plan pl = make_plan(*d, xy != nullptr, xz != nullptr, yz != nullptr, tiled_rows(*d), false);
     const size_t need = kCounterBytes + pl.xy_ws + pl.xz_ws + pl.yz_ws;
     if (workspace == nullptr || workspace_bytes < need)
         return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
 
-    char *ws = static_cast<char *>(workspace);
-    unsigned int *counters = reinterpret_cast<unsigned int *>(ws);
-    ws += kCounterBytes;
+    char *ws = static_cast<char *>(workspace) + kCounterBytes;
     void *xy_dst = pl.xy_ws ? (void *)ws : xy;
     void *xz_dst = pl.xz_ws ? (void *)(ws + pl.xy_ws) : xz;
     void *yz_dst = pl.yz_ws ? (void *)(ws + pl.xy_ws + pl.xz_ws) : yz;
     const int xy_acc = (pl.xy_ws == 0 && (d->flags & SSB_FLAG_XY_ACCUMULATE)) ? 1 : 0;
-
-    if (use_tma) {
-        profile_begin(st);
-        const int rc = launch_deskew_tma(*d, raw, vol, xy_dst, xz_dst, yz_dst, counters, pl.UT, pl.XT, pl.S,
-                                         pl.chunk, xy_acc, st);
-        profile_end(st);
-        if (rc) return rc;
-    } else {
+    {
         TileParams tp{};
         tp.raw = raw;
         tp.vol = vol;

@@ -19,6 +19,7 @@
 //  * int->double conversion is folded into the products: fma(w, 2^52 + a,
 //    -w*2^52) == fl(w*a) exactly (one rounding), so a voxel costs 2 DFMA + 2 DADD.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <cudaTypedefs.h>
 #include <mutex>
@@ -61,9 +62,9 @@ struct alignas(16) RowP {
 
 struct Params {
     uint16_t *vol;
-    void *xy;
-    void *xz;
-    void *yz;
+    uint32_t *xy;  // u32 reduction targets (zeroed, or the caller's sum outputs)
+    uint32_t *xz;
+    uint32_t *yz;
     unsigned int *counters;  // [0] next item (zeroed by the host before the launch)
     int64_t n, h, w, first, u_begin, u_count, chunk;
     double shear;
@@ -132,6 +133,34 @@ __device__ __forceinline__ uint4 voxels8(const uint4 a, const uint4 b, const Row
         o[q] = __byte_perm(lo, hi, 0x5410);
     }
     return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// 8 packed uint16 -> 8 doubles 2^52 + v (exact; one integer op + the constant high word each)
+__device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
+    const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        o[2 * q] = biased(w4[q] & 0xFFFFu);
+        o[2 * q + 1] = biased(w4[q] >> 16);
+    }
+}
+
+// canvas lerp of 8 voxels from biased taps: rint(fl(fl(w0*a) + fl(f*b)))
+__device__ __forceinline__ uint4 lerp_biased8(const double (&a)[8], const double (&b)[8], const double c0,
+                                              const double c1, const double n0, const double n1) {
+    uint32_t r[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        r[c] = (uint32_t)__double2loint(
+            __dadd_rn(__dadd_rn(__fma_rn(c0, a[c], n0), __fma_rn(c1, b[c], n1)), kRintMagic));
+    return make_uint4(__byte_perm(r[0], r[1], 0x5410), __byte_perm(r[2], r[3], 0x5410),
+                      __byte_perm(r[4], r[5], 0x5410), __byte_perm(r[6], r[7], 0x5410));
+}
+
+template <bool kMax>
+__device__ __forceinline__ void red_u32(uint32_t *p, uint32_t v) {
+    if (kMax) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    else asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -249,14 +278,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     live_lo = __ballot_sync(0xffffffffu, l0);
                     live_hi = __ballot_sync(0xffffffffu, l1);
                 }
-                if (lane == 0) {
-                    const uint64_t live = (uint64_t)live_lo | ((uint64_t)live_hi << 32);
-                    uint32_t mask = 0;
+                __syncwarp();
+                // per consumer warp: any live row (bits 0..14); all four rows live with
+                // chained taps, off_b(k) == off_a(k+1), so tap rows can be converted once
+                // and reused by the next row (bits 17..31, canvas formula only)
+                const uint64_t live = (uint64_t)live_lo | ((uint64_t)live_hi << 32);
+                bool any = false, chained = false;
+                if (lane < kConsumerWarps) {
+                    const uint32_t bits = (uint32_t)(live >> (lane * kRows)) & ((1u << kRows) - 1);
+                    any = bits != 0;
+                    if (INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS && bits == (1u << kRows) - 1) {
+                        const RowP *g = &sm.rows[stage][lane * kRows];
+                        chained = true;
 #pragma unroll
-                    for (int w = 0; w < kConsumerWarps; ++w)
-                        if ((live >> (w * kRows)) & ((1u << kRows) - 1)) mask |= 1u << w;
-                    sm.hdr[stage] = mask | (hit ? (1u << 16) : 0u);
+                        for (int k = 0; k + 1 < kRows; ++k) chained &= g[k].off_b == g[k + 1].off_a;
+                    }
                 }
+                const uint32_t any_mask = __ballot_sync(0xffffffffu, any);
+                const uint32_t chain_mask = __ballot_sync(0xffffffffu, chained);
+                if (lane == 0) sm.hdr[stage] = any_mask | (hit ? (1u << 16) : 0u) | (chain_mask << 17);
                 __syncwarp();
                 if (lane == 0) {
                     if (hit) {
@@ -320,21 +360,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t xz_sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             uint32_t yzv[kRows] = {0, 0, 0, 0};
             if (live) {
+                const RowP *rg = &sm.rows[stage][warp * kRows];
+                uint4 vs[kRows];
+                if (INTERP == SSB_INTERP_NEAREST) {
+#pragma unroll
+                    for (int k = 0; k < kRows; ++k) vs[k] = lds128(rg[k].off_a + lane_off);
+                } else if (FORMULA == SSB_FORMULA_CANVAS && ((hdr >> (17 + warp)) & 1u)) {
+                    // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
+                    double prev[8];
+                    to_biased8(lds128(rg[0].off_a + lane_off), prev);
+#pragma unroll
+                    for (int k = 0; k < kRows; ++k) {
+                        double cur[8];
+                        to_biased8(lds128(rg[k].off_b + lane_off), cur);
+                        vs[k] = lerp_biased8(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1);
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) prev[c] = cur[c];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kRows; ++k) {
+                        const uint4 a = lds128(rg[k].off_a + lane_off);
+                        const uint4 b = lds128(rg[k].off_b + lane_off);
+                        vs[k] = voxels8<FORMULA>(a, b, rg[k]);
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < kRows; ++k) {
-                    const RowP &rp = sm.rows[stage][warp * kRows + k];
-                    const uint4 a = lds128(rp.off_a + lane_off);
-                    uint4 v;
-                    if (INTERP == SSB_INTERP_NEAREST) {
-                        v = a;
-                    } else {
-                        const uint4 b = lds128(rp.off_b + lane_off);
-                        v = voxels8<FORMULA>(a, b, rp);
-                    }
+                    const uint4 v = vs[k];
                     if (vrow != nullptr && k < rows_ok && col_ok) stg_cs_v4(vrow + (size_t)k * p.w, v);
                     if (kMax) {
                         acc_max[k] = max_u16x8(acc_max[k], v);
-                        xz_max = max_u16x8(xz_max, v);
                         if (p.yz != nullptr) yzv[k] = __reduce_max_sync(0xffffffffu, hmax8(v));
                     } else {
                         const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
@@ -349,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (p.yz != nullptr) yzv[k] = __reduce_add_sync(0xffffffffu, rs);
                     }
                 }
+                if (kMax) xz_max = max_u16x8(max_u16x8(vs[0], vs[1]), max_u16x8(vs[2], vs[3]));
             } else if (vrow != nullptr && col_ok) {
                 const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -362,9 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
             if (p.yz != nullptr && lane < rows_ok) {
                 const uint32_t val = lane == 0 ? yzv[0] : lane == 1 ? yzv[1] : lane == 2 ? yzv[2] : yzv[3];
-                const size_t idx = yz_base + (size_t)(s - s_begin) * p.u_count + lane;
-                if (kMax) static_cast<uint16_t *>(p.yz)[idx] = (uint16_t)val;
-                else static_cast<uint32_t *>(p.yz)[idx] = val;
+                if (val != 0) red_u32<kMax>(p.yz + ((size_t)s * p.u_count + r0 + lane), val);
             }
 
             if (p.xz != nullptr) {
@@ -391,8 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int w2 = 0; w2 < kConsumerWarps; ++w2)
                                 red = __vmaxu2(red, sm.xz[((buf * 2 + gg) * kConsumerWarps + w2) * (kTX / 2) + c2]);
-                            uint16_t *dst = static_cast<uint16_t *>(p.xz) + ((size_t)ut * p.n + s0 + gg) * p.w + col;
-                            *reinterpret_cast<uint32_t *>(dst) = red;
+                            uint32_t *dst = p.xz + (size_t)(s0 + gg) * p.w + col;
+                            if (red & 0xFFFFu) red_u32<true>(dst, red & 0xFFFFu);
+                            if (red >> 16) red_u32<true>(dst + 1, red >> 16);
                         }
                     } else if (tid < kTX) {
                         const int64_t col = (int64_t)xt * kTX + tid;
@@ -400,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             uint32_t red = 0;
 #pragma unroll
                             for (int w2 = 0; w2 < kConsumerWarps; ++w2) red += sm.xz[(buf * kConsumerWarps + w2) * kTX + tid];
-                            static_cast<uint32_t *>(p.xz)[((size_t)ut * p.n + s0) * p.w + col] = red;
+                            if (red) red_u32<false>(p.xz + (size_t)s0 * p.w + col, red);
                         }
                     }
                     ++xz_batch;
@@ -409,30 +465,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         if (p.xy != nullptr && col_ok) {
-            const size_t base = (size_t)sc * plane + (size_t)r0 * p.w + x;
+            uint32_t *base = p.xy + (size_t)r0 * p.w + x;
 #pragma unroll
             for (int k = 0; k < kRows; ++k) {
                 if (k >= rows_ok) break;
+                uint32_t *dst = base + (size_t)k * p.w;
                 if (kMax) {
-                    uint16_t *dst = static_cast<uint16_t *>(p.xy) + base + (size_t)k * p.w;
-                    uint4 v = acc_max[k];
-                    if (p.xy_accumulate) v = max_u16x8(v, *reinterpret_cast<const uint4 *>(dst));
-                    *reinterpret_cast<uint4 *>(dst) = v;
-                } else {
-                    uint32_t *dst = static_cast<uint32_t *>(p.xy) + base + (size_t)k * p.w;
-                    uint4 v0 = make_uint4(acc_sum[k][0], acc_sum[k][1], acc_sum[k][2], acc_sum[k][3]);
-                    uint4 v1 = make_uint4(acc_sum[k][4], acc_sum[k][5], acc_sum[k][6], acc_sum[k][7]);
-                    if (p.xy_accumulate) {
-                        const uint4 o0 = *reinterpret_cast<const uint4 *>(dst);
-                        const uint4 o1 = *reinterpret_cast<const uint4 *>(dst + 4);
-                        v0 = make_uint4(v0.x + o0.x, v0.y + o0.y, v0.z + o0.z, v0.w + o0.w);
-                        v1 = make_uint4(v1.x + o1.x, v1.y + o1.y, v1.z + o1.z, v1.w + o1.w);
+                    const uint32_t w4[4] = {acc_max[k].x, acc_max[k].y, acc_max[k].z, acc_max[k].w};
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint32_t e = (w4[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                        if (e) red_u32<true>(dst + c, e);
                     }
-                    *reinterpret_cast<uint4 *>(dst) = v0;
-                    *reinterpret_cast<uint4 *>(dst + 4) = v1;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        if (acc_sum[k][c]) red_u32<false>(dst + c, acc_sum[k][c]);
                 }
             }
         }
+    }
+}
+
+// u32 reduction scratch -> uint16 projections (max mode); dst = max(dst, src) when accumulating.
+struct U16Seg {
+    const uint32_t *src;
+    uint16_t *dst;
+    int64_t count;
+    int32_t accumulate;
+};
+
+__global__ void finalize_u16_kernel(U16Seg s0, U16Seg s1, U16Seg s2) {
+    const int64_t total = s0.count + s1.count + s2.count;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const U16Seg &sg = e < s0.count ? s0 : (e < s0.count + s1.count ? s1 : s2);
+        const int64_t i = e < s0.count ? e : (e < s0.count + s1.count ? e - s0.count : e - s0.count - s1.count);
+        uint32_t v = sg.src[i];
+        if (sg.accumulate) v = max(v, (uint32_t)sg.dst[i]);
+        sg.dst[i] = (uint16_t)v;
     }
 }
 
@@ -468,10 +538,30 @@ bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol
     return tma_path::encode_fn() != nullptr;
 }
 
-int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz,
-                      void *yz, unsigned int *counters, int64_t UT, int64_t XT, int64_t S, int64_t chunk,
-                      int xy_accumulate, cudaStream_t st) {
+namespace {
+constexpr size_t kCounterBytes = 256;
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+int64_t env_i64(const char *name, int64_t dflt) {
+    const char *v = getenv(name);
+    return v ? atoll(v) : dflt;
+}
+}  // namespace
+
+size_t tma_workspace_bytes(const ssb_deskew_desc &d) {
+    // u32 reduction scratch for max mode (sum mode reduces straight into the caller's u32 outputs)
+    size_t b = kCounterBytes;
+    if (d.reduce == SSB_REDUCE_MAX)
+        b += align256((size_t)d.u_count * d.width * 4) + align256((size_t)d.n * d.width * 4) +
+             align256((size_t)d.n * d.u_count * 4);
+    return b;
+}
+
+int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz, void *yz,
+                      void *workspace, size_t workspace_bytes, cudaStream_t st) {
     using namespace tma_path;
+    if (workspace == nullptr || workspace_bytes < tma_workspace_bytes(d))
+        return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", tma_workspace_bytes(d),
+                    workspace_bytes);
     CUtensorMap map;
     const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)d.n};
     const cuuint64_t strides[2] = {(cuuint64_t)d.width * 2, (cuuint64_t)d.width * d.height * 2};
@@ -481,14 +571,49 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(SSB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    const int64_t items = UT * XT * S;
+
+    // work items: (u-tile, x-tile, slice chunk); ~kItemsPerCta items per persistent CTA keep the
+    // dynamic scheduler's tail short (projections reduce in L2, so chunking costs no partial planes)
+    const int sms = num_sms();
+    const int64_t UT = std::max<int64_t>(1, (d.u_count + kTU - 1) / kTU);
+    const int64_t XT = std::max<int64_t>(1, (d.width + kTX - 1) / kTX);
+    const int64_t tiles = UT * XT;
+    const int64_t want = env_i64("SSB_ITEMS_PER_CTA", 12) * sms;
+    int64_t S = std::max<int64_t>(1, std::min<int64_t>(d.n, (want + tiles - 1) / tiles));
+    const int64_t chunk = std::max<int64_t>(1, (d.n + S - 1) / S);
+    S = (d.n + chunk - 1) / chunk;
+    const int64_t items = tiles * S;
     if (items > INT32_MAX / 2) return fail(SSB_ERR_CAPACITY, "too many tiles");
+
+    char *ws = static_cast<char *>(workspace);
+    unsigned int *counters = reinterpret_cast<unsigned int *>(ws);
+    ws += kCounterBytes;
+    const bool mx = d.reduce == SSB_REDUCE_MAX;
+    const bool acc = (d.flags & SSB_FLAG_XY_ACCUMULATE) != 0;
+    const size_t n_xy = (size_t)d.u_count * d.width, n_xz = (size_t)d.n * d.width, n_yz = (size_t)d.n * d.u_count;
+    uint32_t *xy32 = nullptr, *xz32 = nullptr, *yz32 = nullptr;
+    if (mx) {
+        xy32 = xy ? reinterpret_cast<uint32_t *>(ws) : nullptr;
+        ws += align256(n_xy * 4);
+        xz32 = xz ? reinterpret_cast<uint32_t *>(ws) : nullptr;
+        ws += align256(n_xz * 4);
+        yz32 = yz ? reinterpret_cast<uint32_t *>(ws) : nullptr;
+    } else {
+        xy32 = static_cast<uint32_t *>(xy);
+        xz32 = static_cast<uint32_t *>(xz);
+        yz32 = static_cast<uint32_t *>(yz);
+    }
+    cudaMemsetAsync(counters, 0, sizeof(unsigned int), st);
+    if (xy32 && (mx || !acc)) cudaMemsetAsync(xy32, 0, n_xy * 4, st);
+    if (xz32) cudaMemsetAsync(xz32, 0, n_xz * 4, st);
+    if (yz32) cudaMemsetAsync(yz32, 0, n_yz * 4, st);
+    if (int rc = check_launch("ssb_deskew scratch reset")) return rc;
 
     Params prm{};
     prm.vol = vol;
-    prm.xy = xy;
-    prm.xz = xz;
-    prm.yz = yz;
+    prm.xy = xy32;
+    prm.xz = xz32;
+    prm.yz = yz32;
     prm.counters = counters;
     prm.n = d.n;
     prm.h = d.height;
@@ -502,13 +627,11 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     prm.XT = (int32_t)XT;
     prm.S = (int32_t)S;
     prm.n_items = (int32_t)items;
-    prm.xy_accumulate = xy_accumulate;
-    const int grid = (int)std::min<int64_t>(items, num_sms());
-    if (cudaMemsetAsync(counters, 0, sizeof(unsigned int), st) != cudaSuccess)
-        return fail(SSB_ERR_CUDA, "scheduler counter reset failed");
+    prm.xy_accumulate = acc;
+    const int grid = (int)std::min<int64_t>(items, sms);
 
     int rc;
-    const bool mx = d.reduce == SSB_REDUCE_MAX;
+    profile_begin(st);
     if (d.interp == SSB_INTERP_NEAREST)
         rc = mx ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX>(map, prm, grid, st)
                 : launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM>(map, prm, grid, st);
@@ -518,8 +641,21 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     else
         rc = mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_MAX>(map, prm, grid, st)
                 : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM>(map, prm, grid, st);
+    profile_end(st);
     count_launches(1);
-    return rc;
+    if (rc) return rc;
+
+    if (mx && (xy32 || xz32 || yz32)) {
+        U16Seg a{xy32, static_cast<uint16_t *>(xy), xy32 ? (int64_t)n_xy : 0, acc ? 1 : 0};
+        U16Seg b{xz32, static_cast<uint16_t *>(xz), xz32 ? (int64_t)n_xz : 0, 0};
+        U16Seg c{yz32, static_cast<uint16_t *>(yz), yz32 ? (int64_t)n_yz : 0, 0};
+        const int64_t total = a.count + b.count + c.count;
+        const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+        finalize_u16_kernel<<<blocks, 256, 0, st>>>(a, b, c);
+        count_launches(1);
+        return check_launch("finalize_u16_kernel");
+    }
+    return SSB_OK;
 }
 
 }  // namespace ssb

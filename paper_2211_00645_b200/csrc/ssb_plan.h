@@ -14,9 +14,11 @@ constexpr int kTmaTileCols = 256;  // columns per work item (32 lanes x 8)
 // TMA path usable for this call (16-byte aligned buffers, W % 8 == 0, driver entry point found)?
 bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol, const void *xy);
 
-// Launch the persistent TMA kernel; counters: >= 4 bytes of device scratch.
-int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz,
-                      void *yz, unsigned int *counters, int64_t UT, int64_t XT, int64_t S, int64_t chunk,
-                      int xy_accumulate, cudaStream_t st);
+// Workspace the TMA path needs (scheduler counter + u32 reduction scratch for max mode).
+size_t tma_workspace_bytes(const ssb_deskew_desc &d);
+
+// Launch the persistent TMA kernel (+ scratch resets and the u32 -> u16 finalize).
+int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz, void *yz,
+                      void *workspace, size_t workspace_bytes, cudaStream_t st);
 
 }  // namespace ssb
