@@ -36,13 +36,25 @@ namespace tma_path {
 constexpr int kConsumerWarps = 15;  // + 1 producer = 16 warps: 128 registers per thread
 constexpr int kRows = 4;            // canvas rows per consumer warp
 constexpr int kTU = kConsumerWarps * kRows;
-constexpr int kBoxRows = kTU + 4;  // 2 rows of slack on each side of the tile
+constexpr int kBoxRows = kTU + 4;  // smem rows per stage (the largest box below)
+
+// Frame rows a tile needs (box height) and the slack above its first row:
+//   nearest   rows u - lo exactly                      -> TU rows, slack 0
+//   canvas    j0 in {u-b-1, u-b}, j1 <= u-b+1, b = floor(off) -> TU+2 rows, slack 1
+//   npinterp  j = max{k: fl(off+k) <= u} may move +-1 more    -> TU+4 rows, slack 2
+template <int INTERP, int FORMULA>
+__host__ __device__ constexpr int box_slack() {
+    return INTERP == SSB_INTERP_NEAREST ? 0 : (FORMULA == SSB_FORMULA_CANVAS ? 1 : 2);
+}
+template <int INTERP, int FORMULA>
+__host__ __device__ constexpr int box_rows() {
+    return kTU + 2 * box_slack<INTERP, FORMULA>();
+}
 constexpr int kTX = 256;
 constexpr int kStages = 5;
 constexpr int kQueue = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr uint32_t kBoxBytes = kBoxRows * kTX * 2;
 constexpr uint32_t kRowBytes = kTX * 2;
 constexpr int kXzWords = 2 * 2 * kConsumerWarps * (kTX / 2);  // 2 buffers x 2 slices x warps x u16x2
 
@@ -258,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 slice_span(p.first + s, p.shear, p.h, INTERP, lo, hi, off);
                 const bool hit = !(hi < tu0 || lo > tu0 + kTU - 1);
                 const int64_t base = INTERP == SSB_INTERP_NEAREST ? lo : (int64_t)floor(off);
-                const int64_t box_r0 = tu0 - base - 2;
+                const int64_t box_r0 = tu0 - base - box_slack<INTERP, FORMULA>();
                 if (lane == 0) mbar_wait(&sm.empty[stage], sphase ^ 1);
                 __syncwarp();
                 uint32_t live_lo = 0, live_hi = 0;
@@ -300,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) {
                     if (hit) {
-                        mbar_arrive_expect_tx(&sm.full[stage], kBoxBytes);
+                        mbar_arrive_expect_tx(&sm.full[stage], box_rows<INTERP, FORMULA>() * kTX * 2);
                         tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
                                     (int32_t)s, policy);
                     } else {
@@ -495,15 +507,35 @@ struct U16Seg {
     int32_t accumulate;
 };
 
-__global__ void finalize_u16_kernel(U16Seg s0, U16Seg s1, U16Seg s2) {
-    const int64_t total = s0.count + s1.count + s2.count;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const U16Seg &sg = e < s0.count ? s0 : (e < s0.count + s1.count ? s1 : s2);
-        const int64_t i = e < s0.count ? e : (e < s0.count + s1.count ? e - s0.count : e - s0.count - s1.count);
+__device__ __forceinline__ void finalize_seg(const U16Seg &sg, int64_t tid, int64_t nthreads) {
+    // 4 elements per step: one 16-byte load of u32, one 8-byte store of u16 (counts are multiples
+    // of 8 on this path because W % 8 == 0; a scalar tail covers the rest)
+    const int64_t n4 = (reinterpret_cast<uintptr_t>(sg.dst) & 7u) ? 0 : sg.count / 4;
+    const uint4 *src = reinterpret_cast<const uint4 *>(sg.src);
+    uint2 *dst = reinterpret_cast<uint2 *>(sg.dst);
+    for (int64_t i = tid; i < n4; i += nthreads) {
+        const uint4 v = src[i];
+        uint32_t lo = v.x | (v.y << 16), hi = v.z | (v.w << 16);
+        if (sg.accumulate) {
+            const uint2 o = dst[i];
+            lo = __vmaxu2(lo, o.x);
+            hi = __vmaxu2(hi, o.y);
+        }
+        dst[i] = make_uint2(lo, hi);
+    }
+    for (int64_t i = 4 * n4 + tid; i < sg.count; i += nthreads) {
         uint32_t v = sg.src[i];
         if (sg.accumulate) v = max(v, (uint32_t)sg.dst[i]);
         sg.dst[i] = (uint16_t)v;
     }
+}
+
+__global__ void finalize_u16_kernel(U16Seg s0, U16Seg s1, U16Seg s2) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    finalize_seg(s0, tid, nthreads);
+    finalize_seg(s1, tid, nthreads);
+    finalize_seg(s2, tid, nthreads);
 }
 
 // --------------------------------------------------------------------------- host
@@ -565,7 +597,10 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     CUtensorMap map;
     const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)d.n};
     const cuuint64_t strides[2] = {(cuuint64_t)d.width * 2, (cuuint64_t)d.width * d.height * 2};
-    const cuuint32_t box[3] = {(cuuint32_t)kTX, (cuuint32_t)kBoxRows, 1};
+    const int rows = d.interp == SSB_INTERP_NEAREST ? box_rows<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
+                     : d.formula == SSB_FORMULA_CANVAS ? box_rows<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>()
+                                                       : box_rows<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>();
+    const cuuint32_t box[3] = {(cuuint32_t)kTX, (cuuint32_t)rows, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t *>(raw), dims,
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -649,8 +684,8 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
         U16Seg a{xy32, static_cast<uint16_t *>(xy), xy32 ? (int64_t)n_xy : 0, acc ? 1 : 0};
         U16Seg b{xz32, static_cast<uint16_t *>(xz), xz32 ? (int64_t)n_xz : 0, 0};
         U16Seg c{yz32, static_cast<uint16_t *>(yz), yz32 ? (int64_t)n_yz : 0, 0};
-        const int64_t total = a.count + b.count + c.count;
-        const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+        const int64_t total = (a.count + b.count + c.count) / 4;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8));
         finalize_u16_kernel<<<blocks, 256, 0, st>>>(a, b, c);
         count_launches(1);
         return check_launch("finalize_u16_kernel");
