@@ -218,12 +218,12 @@ def run_ours(args, cfg, rank, world, local_rank):
     projs = {0: torch.empty((u, w), dtype=torch.uint16, device=dev),
              1: torch.empty((n, w), dtype=torch.uint16, device=dev),
              2: torch.empty((n, u), dtype=torch.uint16, device=dev)}
-    gather = [torch.empty((u, w), dtype=torch.int16, device=dev) for _ in range(world)] if world > 1 and rank == 0 else None
+    gather = [torch.empty((u, 2 * w), dtype=torch.uint8, device=dev) for _ in range(world)] if world > 1 and rank == 0 else None
 
     def step():
         deskew_device(raw, s, interp, reduce=reduce, volume=vol, projections=projs, stream=stream)
         if world > 1:
-            dist.gather(projs[0].view(torch.int16), gather, dst=0)
+            dist.gather(projs[0].view(torch.uint8), gather, dst=0)
 
     for _ in range(args.warmup):
         step()
