@@ -30,13 +30,16 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 CONFIGS = {
     1: dict(n=128, h=256, w=512, alpha=30.0, name="config1_128x256x512_30deg"),
     2: dict(n=512, h=2048, w=2048, alpha=30.0, name="config2_512x2048x2048_30deg"),
-    3: dict(n=200, h=1024, w=1024, alpha=30.0, name="config3_200x1024x1024_30deg"),
+    3: dict(n=200, h=1024, w=1024, alpha=30.0, name="config3_200x1024x1024_30deg_live_stream"),
+    5: dict(n=8192, h=2048, w=2048, alpha=45.0, name="config5_8192x2048x2048_45deg_slabs_sum"),
 }
 PITCH = STEP = 0.115
 
@@ -332,6 +335,148 @@ def run_ours(args, cfg, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def run_stream(args, cfg, rank, world, local_rank):
+    """Config 3: continuous live-view stacks through the pinned multi-stream H2D pipeline.
+
+    Every step streams one 200 x 1024 x 1024 stack from pinned host memory (chunks on
+    two copy streams, deskew per chunk on the compute stream, XY/XZ/YZ max projections,
+    no volume) and copies the projections back.  Throughput = stacks/s over K
+    back-to-back stacks; latency = last chunk handed to the copy engine -> projections
+    in host memory (the reference's lag_ms, ss/pipeline.py:973), measured per stack.
+    """
+    import torch
+
+    from paper_2211_00645_b200 import _lib
+    from paper_2211_00645_b200.stream import StackStreamer, pinned_stack
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n, h, w = cfg["n"], cfg["h"], cfg["w"]
+    s = native_shear(cfg["alpha"])
+    u = canvas_rows(n, h, s)
+    host = pinned_stack(n, h, w)
+    host[:] = np.random.default_rng(rank).integers(0, 4096, size=(n, h, w), dtype=np.uint16)
+    streamer = StackStreamer(h, w, device=dev, chunk_frames=args.chunk_frames or None)
+    outs = {0: torch.empty((u, w), dtype=torch.uint16, pin_memory=True),
+            1: torch.empty((n, w), dtype=torch.uint16, pin_memory=True),
+            2: torch.empty((n, u), dtype=torch.uint16, pin_memory=True)}
+    cur = torch.cuda.current_stream(dev)
+
+    def step():
+        res = streamer.run(host, s, args.interp, reduce="max", write_volume=False)
+        for a, t in res.projections.items():
+            outs[a].copy_(t, non_blocking=True)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    for _ in range(args.steps):
+        step()
+    e1.record(cur)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = _lib.launch_count() - launches0
+    # latency: one stack at a time; event on the copy stream just before the last chunk
+    lats = []
+    for _ in range(min(args.steps, 10)):
+        torch.cuda.synchronize()
+        streamer.last_chunk_event = torch.cuda.Event(enable_timing=True)
+        step()
+        done = torch.cuda.Event(enable_timing=True)
+        done.record(cur)
+        done.synchronize()
+        lats.append(streamer.last_chunk_event.elapsed_time(done))
+    lat = sorted(lats)[len(lats) // 2]
+    vox = n * u * w
+    if rank == 0:
+        print(json.dumps({
+            "metric": "deskewed GVoxels/s and stacks/s (live-view stream, pinned H2D)", "value": world * vox / (ms * 1e-3) / 1e9,
+            "unit": "GVoxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 in / f64 lerp / u16 out",
+            "data": "synthetic uniform [0,4096) in pinned host memory",
+            "config": {"workload": cfg["name"], "interp": args.interp, "canvas": [u, w], "stacks_per_s": 1e3 / ms,
+                       "latency_ms_last_chunk_to_host": lat, "chunk_frames": streamer.chunk,
+                       "outputs": "XY/XZ/YZ max to host every stack, no volume",
+                       "h2d_GBps": 2 * n * h * w / (ms * 1e-3) / 1e9},
+            "gpu_launches": launches,
+        }), flush=True)
+
+
+def run_slabs(args, cfg, rank, world, local_rank):
+    """Config 5: one 8192-frame scan split into contiguous scan-axis slabs (strong scaling).
+
+    Rank r deskews frames [first, first+count) with global slice indices over its canvas
+    row window, projection-only, sum XY (uint32); the partial canvases are merged on rank 0
+    with one NCCL reduce (int64 sum) inside the timed step.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from paper_2211_00645_b200 import _lib
+    from paper_2211_00645_b200 import dist as D
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n, h, w = cfg["n"], cfg["h"], cfg["w"]
+    s = native_shear(cfg["alpha"])
+    plans = D.plan_slabs(n, h, s, args.interp, world)
+    p = plans[rank]
+    g = torch.Generator(device=dev).manual_seed(77 + rank)
+    raw = torch.empty((p.count, h, w), dtype=torch.uint16, device=dev)
+    for k in range(0, p.count, 64):  # generate in chunks (no 2x int32 temporary of the whole slab)
+        m = min(64, p.count - k)
+        raw[k:k + m] = torch.randint(0, 4096, (m, h, w), generator=g, device=dev, dtype=torch.int32).to(torch.uint16)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        res = D.deskew_slab(raw, p, s, args.interp, reduce="sum", projection_axes=(0,), stream=stream)
+        if world > 1:
+            D.combine_xy(res.projections[0], p, w, "sum")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = _lib.launch_count()
+    _lib.profile_enable(True)
+    _lib.profile_read()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    _lib.profile_enable(False)
+    kern_ms, kern_n = _lib.profile_read()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    U = p.canvas_rows
+    vox = n * U * w
+    bytes_launch = 2 * p.count * h * w + 4 * p.u_count * w
+    peak, peak_kind = peaks()
+    achieved = bytes_launch / (kern_ms / max(kern_n, 1) * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": "deskewed GVoxels/s (long scan, scan-axis slabs, sum projection)", "value": vox / (ms * 1e-3) / 1e9,
+            "unit": "GVoxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16 in / f64 lerp / u32 sum",
+            "data": "synthetic uniform [0,4096), generated on device",
+            "config": {"workload": cfg["name"], "interp": args.interp, "canvas": [U, w],
+                       "slab_frames": p.count, "slab_rows": p.u_count, "outputs": "XY sum only (projection-only)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "peak_kind": peak_kind, "bytes_per_launch": bytes_launch,
+                         "kernel_ms": kern_ms / max(kern_n, 1)},
+            "gpu_launches": _lib.launch_count() - launches0,
+        }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -346,6 +491,7 @@ def main():
     ap.add_argument("--warmup-ref", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--chunk-frames", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -363,7 +509,8 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, cfg, rank, world, local_rank)
+        runner = {3: run_stream, 5: run_slabs}.get(args.config, run_ours)
+        runner(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

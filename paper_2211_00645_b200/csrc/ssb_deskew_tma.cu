@@ -219,6 +219,73 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     return true;
 }
 
+__device__ __forceinline__ uint32_t redux_max(uint32_t v) {
+    uint32_t r;
+    asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t redux_add(uint32_t v) {
+    uint32_t r;
+    asm volatile("redux.sync.add.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+// One consumer warp's 4 canvas rows of one slice: sample, store, fold into XY / XZ / YZ.
+// FULL: all 8 columns of every lane and all 4 rows are inside the output (no predicates).
+template <int INTERP, int FORMULA, bool kMax, bool FULL>
+__device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off, const bool chained,
+                                          const bool want_yz, uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
+                                          uint4 (&acc_max)[kRows], uint32_t (&acc_sum)[kMax ? 1 : kRows][8],
+                                          uint4 &xz_max, uint32_t (&xz_sum)[8], uint32_t (&yzv)[kRows]) {
+    uint4 vs[kRows];
+    if (INTERP == SSB_INTERP_NEAREST) {
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) vs[k] = lds128(rg[k].off_a + lane_off);
+    } else if (FORMULA == SSB_FORMULA_CANVAS && chained) {
+        // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
+        double prev[8];
+        to_biased8(lds128(rg[0].off_a + lane_off), prev);
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) {
+            double cur[8];
+            to_biased8(lds128(rg[k].off_b + lane_off), cur);
+            vs[k] = lerp_biased8(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) prev[c] = cur[c];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) {
+            const uint4 a = lds128(rg[k].off_a + lane_off);
+            const uint4 b = lds128(rg[k].off_b + lane_off);
+            vs[k] = voxels8<FORMULA>(a, b, rg[k]);
+        }
+    }
+    const bool store = vrow != nullptr;
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+        const uint4 v = vs[k];
+        if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, v);
+        if (kMax) {
+            acc_max[k] = max_u16x8(acc_max[k], v);
+            if (want_yz) yzv[k] = redux_max(hmax8(v));
+        } else {
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+            uint32_t rs = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t e = (w4[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                acc_sum[k][c] += e;
+                xz_sum[c] += e;
+                rs += e;
+            }
+            if (want_yz) yzv[k] = redux_add(rs);
+        }
+    }
+    if (kMax) xz_max = max_u16x8(max_u16x8(vs[0], vs[1]), max_u16x8(vs[2], vs[3]));
+}
+
 template <int INTERP, int FORMULA, int REDUCE>
 __global__ void __launch_bounds__(kThreads, 1)
     deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
@@ -352,7 +419,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t rows_left = p.u_count - r0;
         const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= kRows ? kRows : (int)rows_left);
         uint16_t *vrow = p.vol != nullptr ? p.vol + (size_t)s_begin * plane + (size_t)r0 * p.w + x : nullptr;
-        const size_t yz_base = ((size_t)xt * p.n + s_begin) * p.u_count + r0;
+        // warp-uniform fast path: every lane's 8 columns and all 4 rows inside the output
+        const bool fast = __all_sync(0xffffffffu, col_ok) && rows_ok == kRows;
+        const bool want_yz = p.yz != nullptr;
 
         uint4 acc_max[kRows];
         uint32_t acc_sum[kMax ? 1 : kRows][8];
@@ -373,51 +442,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t yzv[kRows] = {0, 0, 0, 0};
             if (live) {
                 const RowP *rg = &sm.rows[stage][warp * kRows];
-                uint4 vs[kRows];
-                if (INTERP == SSB_INTERP_NEAREST) {
-#pragma unroll
-                    for (int k = 0; k < kRows; ++k) vs[k] = lds128(rg[k].off_a + lane_off);
-                } else if (FORMULA == SSB_FORMULA_CANVAS && ((hdr >> (17 + warp)) & 1u)) {
-                    // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
-                    double prev[8];
-                    to_biased8(lds128(rg[0].off_a + lane_off), prev);
-#pragma unroll
-                    for (int k = 0; k < kRows; ++k) {
-                        double cur[8];
-                        to_biased8(lds128(rg[k].off_b + lane_off), cur);
-                        vs[k] = lerp_biased8(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1);
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) prev[c] = cur[c];
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < kRows; ++k) {
-                        const uint4 a = lds128(rg[k].off_a + lane_off);
-                        const uint4 b = lds128(rg[k].off_b + lane_off);
-                        vs[k] = voxels8<FORMULA>(a, b, rg[k]);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < kRows; ++k) {
-                    const uint4 v = vs[k];
-                    if (vrow != nullptr && k < rows_ok && col_ok) stg_cs_v4(vrow + (size_t)k * p.w, v);
-                    if (kMax) {
-                        acc_max[k] = max_u16x8(acc_max[k], v);
-                        if (p.yz != nullptr) yzv[k] = __reduce_max_sync(0xffffffffu, hmax8(v));
-                    } else {
-                        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-                        uint32_t rs = 0;
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            const uint32_t e = (w4[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
-                            acc_sum[k][c] += e;
-                            xz_sum[c] += e;
-                            rs += e;
-                        }
-                        if (p.yz != nullptr) yzv[k] = __reduce_add_sync(0xffffffffu, rs);
-                    }
-                }
-                if (kMax) xz_max = max_u16x8(max_u16x8(vs[0], vs[1]), max_u16x8(vs[2], vs[3]));
+                const bool chained = (hdr >> (17 + warp)) & 1u;
+                if (fast)
+                    rows_pass<INTERP, FORMULA, kMax, true>(rg, lane_off, chained, want_yz, vrow, p.w, rows_ok, col_ok, acc_max,
+                                                          acc_sum, xz_max, xz_sum, yzv);
+                else
+                    rows_pass<INTERP, FORMULA, kMax, false>(rg, lane_off, chained, want_yz, vrow, p.w, rows_ok, col_ok, acc_max,
+                                                           acc_sum, xz_max, xz_sum, yzv);
             } else if (vrow != nullptr && col_ok) {
                 const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll

@@ -77,6 +77,9 @@ class StackStreamer:
         self.compute_stream = torch.cuda.Stream(self.device)
         self._done = [None] * self.n_buffers  # compute-finished events per buffer
         self.timings = StreamTimings()
+        #: if set to a timing-enabled torch.cuda.Event, run() records it on the copy stream
+        #: right before the last chunk's H2D copy (end-to-end latency measurement)
+        self.last_chunk_event = None
 
     def _staging_ring(self):
         if self._staging is None:
@@ -128,6 +131,8 @@ class StackStreamer:
                 host = self._staging_ring()[b][:m]
                 host.copy_(src[c0:c1])  # pageable -> pinned (host memcpy)
             with torch.cuda.stream(cs):
+                if c == n_chunks - 1 and self.last_chunk_event is not None:
+                    self.last_chunk_event.record(cs)
                 self.dev_bufs[b][:m].copy_(host, non_blocking=True)
                 copied = torch.cuda.Event()
                 copied.record(cs)
