@@ -329,7 +329,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_launch": bytes_launch, "kernel_ms": kern_avg,
-                         "kernel": "deskew_tiles_kernel"},
+                         "kernel": "deskew_tma_kernel (TMA-pipelined persistent)"},
             "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
