@@ -62,6 +62,8 @@ typedef struct ssb_deskew_desc {
     int64_t u_count;     /* canvas rows covered (volume / XY / YZ row extent)      */
     int32_t reduce;      /* SSB_REDUCE_*                                           */
     int32_t flags;       /* SSB_FLAG_*                                             */
+    int64_t row_stride;  /* elements between frame rows (0: width); lets a channel  */
+    int64_t frame_stride;/* crop of a wider camera frame be deskewed in place (0: H*row_stride) */
 } ssb_deskew_desc;
 
 /* Library version (SSB_VERSION) and the last error message of this thread. */
@@ -88,7 +90,9 @@ size_t ssb_deskew_workspace_bytes(const ssb_deskew_desc *d);
  *   ProjectionCanvas.place x n + finalize_global   ss/pipeline.py:316-336  (formula CANVAS)
  *   phantom.reference_deskew                       ss/phantom.py:359-402   (formula NPINTERP)
  *   _interp_slice_rows per slice                   ss/pipeline.py:229-236
- * raw: device (n, H, W) uint16.  vol: device (n, u_count, W) uint16 or NULL.
+ * raw: device (n, H, W) uint16, row / frame strides from the descriptor (a channel
+ * crop of ss/pipeline.py:105-112 is passed as a strided view, no copy).
+ * vol: device (n, u_count, W) uint16 or NULL.
  * xy (u_count, W), xz (n, W), yz (n, u_count): device, uint16 (max) or
  * uint32 (sum), each may be NULL.  workspace: device, >= ssb_deskew_workspace_bytes.
  * Pointers must be 16-byte aligned for the vectorised path (any alignment works).

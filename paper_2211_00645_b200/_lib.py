@@ -44,6 +44,8 @@ class DeskewDesc(ctypes.Structure):
         ("u_count", ctypes.c_int64),
         ("reduce", ctypes.c_int32),
         ("flags", ctypes.c_int32),
+        ("row_stride", ctypes.c_int64),
+        ("frame_stride", ctypes.c_int64),
     ]
 
 

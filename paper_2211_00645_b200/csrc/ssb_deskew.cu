@@ -41,6 +41,7 @@ struct TileParams {
     void *xz;  // base of XZ planes (UT planes of n*W), or final
     void *yz;  // base of YZ planes (XT planes of n*u_count), or final
     int64_t n, h, w, first, u_begin, u_count, chunk;
+    int64_t row_stride, frame_stride;  // input strides (elements)
     double shear;
     int32_t UT, XT, S;
     int32_t xy_accumulate;
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(kThreads) deskew_tiles_kernel(const TileParams
     const int64_t tile_u1 = tile_u0 + TU - 1;
     const int64_t s_begin = (int64_t)sc * p.chunk;
     const int64_t s_end = min(p.n, s_begin + p.chunk);
-    const size_t frame_elems = (size_t)p.h * (size_t)p.w;
+    const size_t frame_elems = (size_t)p.frame_stride;
 
     // XY accumulators: max -> 8 packed uint16 per row; sum -> 8 uint32 per row
     uint4 acc_max[ROWS];
@@ -138,11 +139,11 @@ __global__ void __launch_bounds__(kThreads) deskew_tiles_kernel(const TileParams
             const bool row_ok = r < p.u_count;
             uint4 v = make_uint4(0, 0, 0, 0);
             if (rp.kind != 0 && col_ok) {
-                const uint4 a = load8<VEC>(frame + (size_t)rp.j0 * p.w, x, p.w);
+                const uint4 a = load8<VEC>(frame + (size_t)rp.j0 * p.row_stride, x, p.w);
                 if (rp.kind == 1) {
                     v = a;
                 } else {
-                    const uint4 b = load8<VEC>(frame + (size_t)rp.j1 * p.w, x, p.w);
+                    const uint4 b = load8<VEC>(frame + (size_t)rp.j1 * p.row_stride, x, p.w);
                     v = lerp8<FORMULA>(a, b, rp);
                 }
             }
@@ -288,6 +289,9 @@ int validate(const ssb_deskew_desc *d) {
         return fail(SSB_ERR_PARAM, "reduce must be max or sum");
     if (d->u_count < 0 || d->u_begin < 0) return fail(SSB_ERR_PARAM, "bad canvas row window");
     if (d->height > INT32_MAX) return fail(SSB_ERR_CAPACITY, "frame height too large");
+    if (d->row_stride != 0 && d->row_stride < d->width) return fail(SSB_ERR_PARAM, "row_stride < width");
+    if (d->frame_stride != 0 && d->frame_stride < row_stride_of(*d) * (d->height - 1) + d->width)
+        return fail(SSB_ERR_PARAM, "frame_stride too small for the frame");
     return SSB_OK;
 }
 
@@ -369,6 +373,8 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
         tp.n = d->n;
         tp.h = d->height;
         tp.w = d->width;
+        tp.row_stride = row_stride_of(*d);
+        tp.frame_stride = frame_stride_of(*d);
         tp.first = d->first_slice;
         tp.u_begin = d->u_begin;
         tp.u_count = d->u_count;
@@ -378,7 +384,8 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
         tp.XT = (int32_t)pl.XT;
         tp.S = (int32_t)pl.S;
         tp.xy_accumulate = xy_acc;
-        const bool vec = (d->width % 8 == 0) && aligned16(raw) && aligned16(vol) &&
+        const bool vec = (d->width % 8 == 0) && (tp.row_stride % 8 == 0) && (tp.frame_stride % 8 == 0) &&
+                         aligned16(raw) && aligned16(vol) &&
                          (d->reduce != SSB_REDUCE_MAX || aligned16(tp.xy));
         const int64_t items = pl.UT * pl.XT * pl.S;
         if (items > INT32_MAX) return fail(SSB_ERR_CAPACITY, "too many tiles");

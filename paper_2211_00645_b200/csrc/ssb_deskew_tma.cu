@@ -597,6 +597,7 @@ int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t
 
 bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol, const void *xy) {
     if (d.width % 8 != 0 || !aligned16(raw) || !aligned16(vol) || !aligned16(xy)) return false;
+    if (row_stride_of(d) % 8 != 0 || frame_stride_of(d) % 8 != 0) return false;  // TMA: 16-byte strides
     if (d.n > INT32_MAX || d.height > INT32_MAX || d.width > INT32_MAX) return false;
     return tma_path::encode_fn() != nullptr;
 }
@@ -627,7 +628,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
                     workspace_bytes);
     CUtensorMap map;
     const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)d.n};
-    const cuuint64_t strides[2] = {(cuuint64_t)d.width * 2, (cuuint64_t)d.width * d.height * 2};
+    const cuuint64_t strides[2] = {(cuuint64_t)row_stride_of(d) * 2, (cuuint64_t)frame_stride_of(d) * 2};
     const int rows = d.interp == SSB_INTERP_NEAREST ? box_rows<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
                      : d.formula == SSB_FORMULA_CANVAS ? box_rows<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>()
                                                        : box_rows<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>();

@@ -11,6 +11,11 @@ namespace ssb {
 constexpr int kTmaTileRows = 60;   // canvas rows per TMA work item (15 consumer warps x 4 rows)
 constexpr int kTmaTileCols = 256;  // columns per work item (32 lanes x 8)
 
+inline int64_t row_stride_of(const ssb_deskew_desc &d) { return d.row_stride ? d.row_stride : d.width; }
+inline int64_t frame_stride_of(const ssb_deskew_desc &d) {
+    return d.frame_stride ? d.frame_stride : row_stride_of(d) * d.height;
+}
+
 // TMA path usable for this call (16-byte aligned buffers, W % 8 == 0, driver entry point found)?
 bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol, const void *xy);
 

@@ -114,12 +114,13 @@ _workspaces = _Workspaces()
 
 
 def make_desc(n, h, w, first_slice, shear_px, interp, formula, u_begin, u_count, reduce,
-              xy_accumulate=False) -> _lib.DeskewDesc:
+              xy_accumulate=False, row_stride=0, frame_stride=0) -> _lib.DeskewDesc:
     return _lib.DeskewDesc(
         n=n, height=h, width=w, first_slice=first_slice, shear_px=float(shear_px),
         interp=_lib.INTERP[interp], formula=_lib.FORMULA[formula], u_begin=u_begin,
         u_count=u_count, reduce=_lib.REDUCE[reduce],
         flags=_lib.FLAG_XY_ACCUMULATE if xy_accumulate else 0,
+        row_stride=row_stride, frame_stride=frame_stride,
     )
 
 
@@ -131,7 +132,9 @@ def deskew_device(raw: torch.Tensor, shear_px: float, interp: str = "linear", *,
                   stream: torch.cuda.Stream | None = None) -> DeskewResult:
     """Fused deskew + projections of device-resident frames (one ``ssb_deskew``).
 
-    raw: CUDA uint16 (n, H, W) contiguous; frame k is global slice first_slice+k.
+    raw: CUDA uint16 (n, H, W); frame k is global slice first_slice+k.  Columns must be
+    contiguous; rows and frames may be strided (a channel crop of a wider camera frame,
+    ss/pipeline.py:105-112, is deskewed in place without a copy).
     Output buffers may be passed in (``volume``, ``projections``) to avoid
     allocation; ``xy_accumulate`` folds into an existing XY (streaming place).
     """
@@ -142,8 +145,14 @@ def deskew_device(raw: torch.Tensor, shear_px: float, interp: str = "linear", *,
         raise ParameterError(f"frame pixels must be uint16, got {raw.dtype}")
     if raw.dim() != 3:
         raise ParameterError("raw must be (n, H, W)")
-    if not raw.is_contiguous():
+    if raw.shape[2] > 1 and raw.stride(2) != 1:
         raw = raw.contiguous()
+    n_, h_, w_ = (int(v) for v in raw.shape)
+    row_stride = int(raw.stride(1)) if h_ > 1 else w_
+    frame_stride = int(raw.stride(0)) if n_ > 1 else row_stride * h_
+    if row_stride < w_ or frame_stride < row_stride * (h_ - 1) + w_:
+        raw = raw.contiguous()
+        row_stride, frame_stride = w_, w_ * h_
     if shear_px < 0:
         raise ParameterError(f"shear_px must be >= 0, got {shear_px}")
     if first_slice < 0:
@@ -175,7 +184,7 @@ def deskew_device(raw: torch.Tensor, shear_px: float, interp: str = "linear", *,
         if volume is not None and (tuple(volume.shape) != (n, u_count, w) or volume.dtype != torch.uint16):
             raise ParameterError(f"volume buffer must be (n, U, W) = {(n, u_count, w)} uint16")
         desc = make_desc(n, h, w, first_slice, shear_px, interp, formula, u_begin, u_count, reduce,
-                         xy_accumulate)
+                         xy_accumulate, row_stride, frame_stride)
         lib = _lib.load()
         ws_bytes = int(lib.ssb_deskew_workspace_bytes(ctypes.byref(desc)))
         ws = _workspaces.get(ws_bytes, stream)

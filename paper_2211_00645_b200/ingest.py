@@ -1,0 +1,151 @@
+"""Stack ingest straight into page-locked memory.
+
+Reads the reference's recorded-stack formats (ss/source.py:321-474):
+
+* raw: concatenated little-endian uint16 frames, with a JSON sidecar ``<stem>.json``
+  holding ``geometry`` (the six SheetGeometry fields), ``timing`` and ``frames``
+  (ss/source.py:321-385);
+* multi-page 16-bit grayscale TIFF with the same sidecar (ss/source.py:388-395, 450-474).
+
+Where the reference materialises a Python list of per-frame copies
+(``_load_raw_frames``, ss/source.py:431-447), raw files are read with one
+``readinto`` into a pinned ``(n, H, W)`` buffer, ready for the asynchronous H2D
+copies of ``stream.StackStreamer``.  Channel crops (ss/pipeline.py:105-112) are
+strided views of the device stack (``channel_views``): ``ssb_deskew`` takes row
+and frame strides, so no per-channel copy is made.  Errors are the reference's
+``MetadataError`` with the same messages.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+from .errors import MetadataError
+from .geometry import SheetGeometry
+
+_GEOMETRY_FIELDS = ("alpha_deg", "scan_step_um", "pixel_pitch_um", "slice_count", "frame_width_px",
+                    "frame_height_px")
+_TIMING_FIELDS = ("exposure_ms", "readout_ms")
+
+
+def sidecar_path(path) -> str:
+    return os.path.splitext(str(path))[0] + ".json"
+
+
+def read_sidecar(path):
+    """(SheetGeometry, timing dict, frames or None) -- ss/source.py:343-374."""
+    sp = sidecar_path(path)
+    if not os.path.exists(sp):
+        raise MetadataError(f"no sidecar file {sp}")
+    with open(sp) as fh:
+        try:
+            data = json.load(fh)
+        except json.JSONDecodeError as exc:
+            raise MetadataError(f"sidecar {sp} is not valid JSON: {exc}") from exc
+    for section, fields in (("geometry", _GEOMETRY_FIELDS), ("timing", _TIMING_FIELDS)):
+        if section not in data:
+            raise MetadataError(f"sidecar missing section '{section}'")
+        for f in fields:
+            if f not in data[section]:
+                raise MetadataError(f"sidecar missing field '{section}.{f}'")
+    g = data["geometry"]
+    geom = SheetGeometry(alpha_deg=g["alpha_deg"], scan_step_um=g["scan_step_um"],
+                         pixel_pitch_um=g["pixel_pitch_um"], slice_count=int(g["slice_count"]),
+                         frame_width_px=int(g["frame_width_px"]), frame_height_px=int(g["frame_height_px"]))
+    t = data["timing"]
+    timing = {"exposure_ms": t["exposure_ms"], "readout_ms": t["readout_ms"],
+              "trigger_mode": t.get("trigger_mode", "internal")}
+    frames = data.get("frames")
+    return geom, timing, None if frames is None else int(frames)
+
+
+def _alloc(n: int, h: int, w: int, pinned: bool) -> np.ndarray:
+    if pinned:
+        from .stream import pinned_stack
+
+        return pinned_stack(n, h, w)
+    return np.empty((n, h, w), dtype=np.uint16)
+
+
+def _load_raw(path, geom: SheetGeometry, count, pinned: bool) -> np.ndarray:
+    w, h = geom.frame_width_px, geom.frame_height_px
+    frame_px = w * h
+    size = os.path.getsize(path)
+    px = size // 2
+    if size % 2 or px == 0 or px % frame_px != 0:
+        raise MetadataError(f"raw file holds {px} pixels, not a multiple of the sidecar frame size {w}x{h}")
+    n = px // frame_px
+    if count is not None and n != count:
+        raise MetadataError(f"raw file holds {n} frames, sidecar says {count}")
+    out = _alloc(n, h, w, pinned)
+    with open(path, "rb", buffering=0) as fh:
+        view = memoryview(out.reshape(-1).view(np.uint8))
+        got = 0
+        while got < size:
+            k = fh.readinto(view[got:])
+            if not k:
+                raise MetadataError(f"short read from {path}")
+            got += k
+    if sys.byteorder == "big":  # the file is little-endian ("<u2", ss/source.py:384)
+        out.byteswap(inplace=True)
+    return out
+
+
+def _load_tiff(path, geom: SheetGeometry, count, pinned: bool) -> np.ndarray:
+    from PIL import Image
+
+    w, h = geom.frame_width_px, geom.frame_height_px
+    try:
+        with Image.open(path) as im:
+            n = getattr(im, "n_frames", 1)
+            if count is not None and n != count:
+                raise MetadataError(f"TIFF holds {n} pages, sidecar says {count}")
+            out = _alloc(n, h, w, pinned)
+            for i in range(n):
+                im.seek(i)
+                arr = np.asarray(im)
+                if arr.dtype.itemsize != 2 or arr.ndim != 2:
+                    raise MetadataError(f"page {i} is not 16-bit grayscale ({arr.dtype}, {arr.ndim}-D)")
+                if arr.shape != (h, w):
+                    raise MetadataError(f"TIFF page {i} is {arr.shape[1]}x{arr.shape[0]}, sidecar says {w}x{h}")
+                out[i] = arr
+    except (OSError, SyntaxError) as exc:
+        raise MetadataError(f"cannot read TIFF {path}: {exc}") from exc
+    return out
+
+
+def load_stack(path, geom: SheetGeometry | None = None, *, pinned: bool = True):
+    """Read a recorded stack -> ((n, H, W) uint16 array, geometry, timing dict).
+
+    ``pinned=True`` (default) returns page-locked memory for the H2D pipeline
+    (needs a CUDA device); flags beat sidecar as in ``open_stack`` (ss/source.py:477-496).
+    """
+    path = str(path)
+    if not os.path.exists(path):
+        raise MetadataError(f"no such stack file: {path}")
+    side_geom, timing, count = None, None, None
+    if geom is None:
+        side_geom, timing, count = read_sidecar(path)
+    elif os.path.exists(sidecar_path(path)):
+        _, timing, count = read_sidecar(path)
+    geom = geom if geom is not None else side_geom
+    if path.lower().endswith((".tif", ".tiff")):
+        stack = _load_tiff(path, geom, count, pinned)
+    else:
+        stack = _load_raw(path, geom, count, pinned)
+    return stack, geom, timing
+
+
+def channel_views(stack_dev, layout) -> dict:
+    """Per-channel crops of a device stack as strided views (no copies).
+
+    ``layout`` is a ``pipeline.ChannelLayout``; returns {channel_id: (n, h, w) view}.
+    Mirrors split_channels (ss/pipeline.py:105-112), which copies every crop.
+    """
+    n, H, W = (int(v) for v in stack_dev.shape)
+    layout.validate_frame(W, H)
+    return {r.channel_id: stack_dev[:, r.y0:r.y0 + r.height, r.x0:r.x0 + r.width] for r in layout.regions}

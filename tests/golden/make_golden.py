@@ -201,6 +201,18 @@ def main():
     roll["count"] = np.int64(k)
     np.savez_compressed(os.path.join(HERE, "rolling.npz"), **roll)
 
+    # ---- recorded-stack files (ss/source.py:377-395) ------------------------
+    from skewstream import source as SRC
+    fdir = os.path.join(HERE, "files")
+    os.makedirs(fdir, exist_ok=True)
+    g = geom(6, 10, 24)
+    frames = rng.integers(0, 65536, size=(6, 10, 24)).astype(np.uint16)
+    SRC.write_stack_raw(os.path.join(fdir, "stack.raw"), list(frames), g)
+    SRC.write_stack_tiff(os.path.join(fdir, "stack.tif"), list(frames), g)
+    np.save(os.path.join(fdir, "frames.npy"), frames)
+    src = SRC.open_stack(os.path.join(fdir, "stack.raw"))
+    np.save(os.path.join(fdir, "replayed.npy"), np.stack([src.next_frame().pixels for _ in range(6)]))
+
 
 if __name__ == "__main__":
     main()

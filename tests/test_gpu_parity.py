@@ -392,3 +392,39 @@ def test_launches_are_counted():
     before = _lib.launch_count()
     run(np.zeros((2, 8, 16), np.uint16), 1.0, "linear")
     assert _lib.launch_count() > before
+
+
+def test_channel_crops_deskew_in_place(kernel_path):
+    """Channel crops (ss/pipeline.py:105-112) passed as strided device views, no copy."""
+    from paper_2211_00645_b200.ingest import channel_views
+
+    rng = np.random.default_rng(17)
+    st = rng.integers(0, 65536, (19, 40, 272)).astype(np.uint16)
+    # channel 0 is unaligned (generic path), channel 1 16-byte aligned (TMA path)
+    layout = pl.ChannelLayout(regions=(pl.ChannelRegion(0, 3, 0, 125, 40), pl.ChannelRegion(1, 136, 4, 136, 33)))
+    views = channel_views(torch.from_numpy(st).to(dev()), layout)
+    for r in layout.regions:
+        v = views[r.channel_id]
+        assert not v.is_contiguous()
+        res = deskew_device(v, 0.8660254037844386, "linear", reduce="max")
+        torch.cuda.synchronize()
+        crop = np.ascontiguousarray(st[:, r.y0:r.y0 + r.height, r.x0:r.x0 + r.width])
+        want_vol, want = C.deskew(crop, 0.8660254037844386, "linear")
+        np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
+        for ax in (0, 1, 2):
+            np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
+
+
+def test_pinned_ingest_feeds_streamer():
+    import os as _os
+
+    from paper_2211_00645_b200.ingest import load_stack
+    from paper_2211_00645_b200.stream import StackStreamer
+
+    stack, geom, _ = load_stack(_os.path.join(GOLDEN, "files", "stack.raw"))
+    assert torch.from_numpy(stack).is_pinned()
+    res = StackStreamer(geom.frame_height_px, geom.frame_width_px, chunk_frames=4).run(stack, 1.3, "linear")
+    torch.cuda.synchronize()
+    want_vol, want = C.deskew(np.ascontiguousarray(stack), 1.3, "linear")
+    np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
+    np.testing.assert_array_equal(res.projections[0].cpu().numpy(), want[0])
