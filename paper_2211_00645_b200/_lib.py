@@ -78,7 +78,7 @@ def load(path: str = LIB_PATH):
         lib.ssb_deskew_workspace_bytes.restype = ctypes.c_size_t
         lib.ssb_deskew.argtypes = [pdesc, p, p, p, p, p, p, ctypes.c_size_t, p]
         lib.ssb_deskew.restype = ctypes.c_int
-        lib.ssb_rolling_band.argtypes = [p, p, i64, i64, i64, d, i32, i64, i64, p, p, i64, p]
+        lib.ssb_rolling_band.argtypes = [p, p, i64, i64, i64, d, i32, i64, i64, p, p, i64, i64, p]
         lib.ssb_rolling_band.restype = ctypes.c_int
         lib.ssb_warp_rows.argtypes = [p, i64, i64, d, p, i64, p]
         lib.ssb_warp_rows.restype = ctypes.c_int

@@ -61,21 +61,55 @@ void profile_end(cudaStream_t st) {
 
 namespace {
 
-// ss/pipeline.py:361-377.  One thread per (row, column) of the band.  Ring slot
-// k holds global slice k; the value it offers row u is the same sampled value
-// place() would use (canvas formula); strict '>' keeps the first maximum in
-// ring order; contributor -1 where every offer is 0 / absent.
+// Value ring slot k offers canvas row u, column x: the sample place() would use
+// (canvas formula, ss/pipeline.py:283-290); 0 when the slot is empty or u is outside
+// its span.
+template <int INTERP>
+__device__ __forceinline__ uint32_t ring_offer(const uint16_t *__restrict__ ring, const uint8_t *__restrict__ present,
+                                               int64_t k, int64_t u, int64_t x, int64_t h, int64_t w, double s) {
+    if (!present[k]) return 0;
+    int64_t klo, khi;
+    double off;
+    slice_span(k, s, h, INTERP, klo, khi, off);
+    if (u < klo || u > khi) return 0;
+    const RowParam rp = row_param<INTERP, SSB_FORMULA_CANVAS>(u, klo, off, h);
+    const uint16_t *frame = ring + (size_t)k * h * w;
+    const uint32_t a = frame[(size_t)rp.j0 * w + x];
+    return rp.kind == 2 ? lerp_voxel<SSB_FORMULA_CANVAS>(a, frame[(size_t)rp.j1 * w + x], rp) : a;
+}
+
+// ss/pipeline.py:361-377.  One thread per (row, column) of the band.  Strict '>' in
+// ring order keeps the first maximum; contributor -1 where every offer is 0.
+//
+// Incremental form (replaced = k >= 0, canvas exact before slot k changed): a voxel
+// whose contributor is not k keeps its maximum unless the new offer v of slot k beats
+// it -- v > best, or v == best > 0 with k earlier in ring order -- which is exactly the
+// full re-max (every other slot's offer is unchanged and <= best, with ties only at
+// later ring indices).  Voxels that k contributed to are re-maxed over the whole ring.
 template <int INTERP>
 __global__ void rolling_band_kernel(const uint16_t *__restrict__ ring, const uint8_t *__restrict__ present,
                                     int64_t n_ring, int64_t h, int64_t w, double s, int64_t lo,
                                     int64_t hi, uint16_t *__restrict__ canvas,
-                                    int16_t *__restrict__ contrib) {
+                                    int16_t *__restrict__ contrib, int64_t replaced) {
     const int64_t total = (hi - lo + 1) * w;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t u = lo + e / w;
         const int64_t x = e % w;
-        // slices whose span can contain u: i*s within [u-H-1, u+1] (exact check below)
+        const size_t idx = (size_t)u * w + x;
+        if (replaced >= 0) {
+            const int32_t who = contrib[idx];
+            if (who != replaced) {
+                const uint32_t best = canvas[idx];
+                const uint32_t v = ring_offer<INTERP>(ring, present, replaced, u, x, h, w, s);
+                if (v > best || (v == best && v > 0 && replaced < who)) {
+                    canvas[idx] = (uint16_t)v;
+                    contrib[idx] = (int16_t)replaced;
+                }
+                continue;
+            }
+        }
+        // slices whose span can contain u: i*s within [u-H-1, u+1] (exact check in ring_offer)
         int64_t k_lo = 0, k_hi = n_ring - 1;
         if (s > 0.0) {
             const double kl = floor(((double)(u - h) - 2.0) / s);
@@ -86,23 +120,14 @@ __global__ void rolling_band_kernel(const uint16_t *__restrict__ ring, const uin
         uint32_t best = 0;
         int32_t who = -1;
         for (int64_t k = k_lo; k <= k_hi; ++k) {
-            if (!present[k]) continue;
-            int64_t klo, khi;
-            double off;
-            slice_span(k, s, h, INTERP, klo, khi, off);
-            if (u < klo || u > khi) continue;
-            const RowParam rp = row_param<INTERP, SSB_FORMULA_CANVAS>(u, klo, off, h);
-            const uint16_t *frame = ring + (size_t)k * h * w;
-            const uint32_t a = frame[(size_t)rp.j0 * w + x];
-            uint32_t v = a;
-            if (rp.kind == 2) v = lerp_voxel<SSB_FORMULA_CANVAS>(a, frame[(size_t)rp.j1 * w + x], rp);
+            const uint32_t v = ring_offer<INTERP>(ring, present, k, u, x, h, w, s);
             if (v > best) {
                 best = v;
                 who = (int32_t)k;
             }
         }
-        canvas[u * w + x] = (uint16_t)best;
-        contrib[u * w + x] = (int16_t)who;
+        canvas[idx] = (uint16_t)best;
+        contrib[idx] = (int16_t)who;
     }
 }
 
@@ -177,7 +202,7 @@ extern "C" int ssb_profile_read(double *total_ms, int64_t *launches) {
 extern "C" int ssb_rolling_band(const uint16_t *ring, const uint8_t *present, int64_t n_ring,
                                 int64_t height, int64_t width, double shear_px, int32_t interp,
                                 int64_t lo, int64_t hi, uint16_t *canvas, int16_t *contributor,
-                                int64_t canvas_rows, void *stream) {
+                                int64_t canvas_rows, int64_t replaced, void *stream) {
     if (n_ring < 1 || height < 1 || width < 1) return fail(SSB_ERR_PARAM, "bad ring shape");
     if (!(shear_px >= 0.0)) return fail(SSB_ERR_PARAM, "shear_px must be >= 0");
     if (interp != SSB_INTERP_NEAREST && interp != SSB_INTERP_LINEAR)
@@ -185,14 +210,15 @@ extern "C" int ssb_rolling_band(const uint16_t *ring, const uint8_t *present, in
     if (lo < 0 || hi >= canvas_rows) return fail(SSB_ERR_CAPACITY, "band %lld..%lld outside %lld-row canvas",
                                                 (long long)lo, (long long)hi, (long long)canvas_rows);
     if (hi < lo) return SSB_OK;
+    if (replaced >= n_ring || n_ring > 32767) return fail(SSB_ERR_PARAM, "ring index out of range");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t total = (hi - lo + 1) * width;
     if (interp == SSB_INTERP_NEAREST)
         rolling_band_kernel<SSB_INTERP_NEAREST><<<grid_for(total, 256), 256, 0, st>>>(
-            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor);
+            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor, replaced);
     else
         rolling_band_kernel<SSB_INTERP_LINEAR><<<grid_for(total, 256), 256, 0, st>>>(
-            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor);
+            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor, replaced);
     count_launches(1);
     return check_launch("rolling_band_kernel");
 }

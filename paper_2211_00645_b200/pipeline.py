@@ -139,6 +139,10 @@ class ProjectionCanvas:
         self._ring_dev = None      # (N, H, W) uint16, allocated on first rolling use
         self._present_dev = None   # (N,) uint8
         self._host_cache = None
+        # True while canvas + contributor equal the full re-max over the ring, so a
+        # rolling_replace can take the O(band) incremental path (see ssb_rolling_band)
+        self._exact = True
+        self._canvas_zero = True
 
     # -- device buffers ------------------------------------------------------
     def _alloc_canvas(self) -> None:
@@ -148,6 +152,10 @@ class ProjectionCanvas:
             self.contributor_device = torch.full((self.height, self.width), -1, dtype=torch.int16,
                                                  device=self._device)
         self._host_cache = None
+        self._canvas_zero = True
+
+    def _ring_empty(self) -> bool:
+        return all(rf is None for rf in self._ring)
 
     def _upload(self, pixels: np.ndarray) -> torch.Tensor:
         host = torch.from_numpy(np.ascontiguousarray(pixels))
@@ -170,6 +178,7 @@ class ProjectionCanvas:
         with torch.cuda.stream(self.stream):
             self.max_pixels_device = torch.from_numpy(arr).to(self._device)
         self._host_cache = None
+        self._exact = self._canvas_zero = False
 
     @property
     def contributor(self) -> np.ndarray:
@@ -183,6 +192,7 @@ class ProjectionCanvas:
         with torch.cuda.stream(self.stream):
             self.contributor_device = torch.from_numpy(arr).to(self._device)
         self._host_cache = None
+        self._exact = self._canvas_zero = False
 
     @property
     def ring(self) -> list:
@@ -192,6 +202,7 @@ class ProjectionCanvas:
     def ring(self, frames) -> None:
         """LivePipeline swaps the ring on a mode change (ss/pipeline.py:864)."""
         self._ring = list(frames)
+        self._exact = self._canvas_zero and self._ring_empty()
         if self._present_dev is not None:
             with torch.cuda.stream(self.stream):
                 self._present_dev.zero_()
@@ -234,6 +245,7 @@ class ProjectionCanvas:
                       stream=self.stream)
         self._placed[frame.slice_index] = True
         self._host_cache = None
+        self._exact = self._canvas_zero = False
         return lo, hi
 
     def place_stack(self, frames: torch.Tensor, first_slice: int = 0) -> None:
@@ -247,6 +259,7 @@ class ProjectionCanvas:
         for i in range(first_slice, first_slice + n):
             self._placed[i] = True
         self._host_cache = None
+        self._exact = self._canvas_zero = False
 
     @property
     def placed_count(self) -> int:
@@ -276,6 +289,8 @@ class ProjectionCanvas:
             self.contributor_device.fill_(-1)
         self._placed = [False] * self.geom.slice_count
         self._host_cache = None
+        self._canvas_zero = True
+        self._exact = self._ring_empty()
 
     # -- rolling mode --------------------------------------------------------------
     def _ring_store(self, frame: RawFrame) -> None:
@@ -295,18 +310,23 @@ class ProjectionCanvas:
         self._ring[frame.slice_index] = frame
         self._ring_store(frame)
         lo, hi = self.row_span(frame.slice_index)
-        self._recompute_band(lo, hi)
+        self._recompute_band(lo, hi, frame.slice_index if self._exact else -1)
         return lo, hi
 
-    def _recompute_band(self, lo: int, hi: int) -> None:
-        """ss/pipeline.py:361-377 on device (strict '>' max, first-max-wins contributor)."""
+    def _recompute_band(self, lo: int, hi: int, replaced: int = -1) -> None:
+        """ss/pipeline.py:361-377 on device (strict '>' max, first-max-wins contributor).
+
+        replaced >= 0 takes the incremental path: exact while the canvas equals the
+        full ring re-max (``_exact``); otherwise the whole band is re-maxed.
+        """
         lib = _lib.load()
         _lib.check(lib.ssb_rolling_band(
             _vp(self._ring_dev), _vp(self._present_dev), self.geom.slice_count,
             self.geom.frame_height_px, self.width, self.shear_px, _lib.INTERP[self.interp], lo, hi,
-            _vp(self.max_pixels_device), _vp(self.contributor_device), self.height,
+            _vp(self.max_pixels_device), _vp(self.contributor_device), self.height, replaced,
             ctypes.c_void_p(self.stream.cuda_stream)))
         self._host_cache = None
+        self._canvas_zero = False
 
     def replace_all(self, shear_px: float | None = None) -> None:
         """Rebuild the canvas, optionally under a new shear (ss/pipeline.py:379-398)."""
@@ -315,6 +335,9 @@ class ProjectionCanvas:
         self.width, self.height = geometry.output_extent(self.geom, self.shear_px, self._pixel_limit)
         self._alloc_canvas()
         self._placed = [False] * self.geom.slice_count
+        # re-adding every live slot in ring order onto a zero canvas with the incremental
+        # rule yields the full re-max (ties keep the earliest slot)
+        self._exact = True
         if self.mode == "rolling":
             for rf in self._ring:
                 if rf is not None:

@@ -428,3 +428,42 @@ def test_pinned_ingest_feeds_streamer():
     want_vol, want = C.deskew(np.ascontiguousarray(stack), 1.3, "linear")
     np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
     np.testing.assert_array_equal(res.projections[0].cpu().numpy(), want[0])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_rolling_incremental_matches_full_remax_with_ties(seed):
+    """Incremental band updates (contributor != replaced slot) vs the reference's full
+    band re-max at every step; values in [0, 4) force many ties and zeros."""
+    rng = np.random.default_rng(500 + seed)
+    n, h, w = int(rng.integers(2, 12)), int(rng.integers(2, 14)), int(rng.integers(1, 40))
+    s = float(rng.choice([0.0, 0.5, 1.0, rng.uniform(0, 2.5)]))
+    interp = str(rng.choice(["nearest", "linear"]))
+    c = pl.ProjectionCanvas(geom(n=n, w=w, h=h), s, interp=interp, mode="rolling")
+    U = c.height
+    ring = [None] * n
+    canvas = np.zeros((U, w), np.uint16)
+    contrib = np.full((U, w), -1, np.int16)
+    for step in range(4 * n):
+        i = int(rng.integers(0, n))
+        px = rng.integers(0, 4, size=(h, w)).astype(np.uint16)
+        ring[i] = px
+        c.rolling_replace(pl.RawFrame(px, i, sweep_index=step // n))
+        lo, hi = O.span(i, s, h, interp)
+        band, cb = O.rolling_band(ring, s, interp, h, w, lo, hi)
+        canvas[lo:hi + 1], contrib[lo:hi + 1] = band, cb
+        np.testing.assert_array_equal(c.max_pixels, canvas)
+        np.testing.assert_array_equal(c.contributor, contrib)
+    # a reset with a non-empty ring forces the full-band path from then on
+    c.reset()
+    canvas[:] = 0
+    contrib[:] = -1
+    for step in range(n):
+        i = int(rng.integers(0, n))
+        px = rng.integers(0, 4, size=(h, w)).astype(np.uint16)
+        ring[i] = px
+        c.rolling_replace(pl.RawFrame(px, i))
+        lo, hi = O.span(i, s, h, interp)
+        band, cb = O.rolling_band(ring, s, interp, h, w, lo, hi)
+        canvas[lo:hi + 1], contrib[lo:hi + 1] = band, cb
+        np.testing.assert_array_equal(c.max_pixels, canvas)
+        np.testing.assert_array_equal(c.contributor, contrib)
