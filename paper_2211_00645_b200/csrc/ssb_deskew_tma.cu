@@ -34,29 +34,42 @@ namespace ssb {
 namespace tma_path {
 
 constexpr int kConsumerWarps = 15;  // + 1 producer = 16 warps: 128 registers per thread
-constexpr int kRows = 4;            // canvas rows per consumer warp
-constexpr int kTU = kConsumerWarps * kRows;
-constexpr int kBoxRows = kTU + 4;  // smem rows per stage (the largest box below)
-
-// Frame rows a tile needs (box height) and the slack above its first row:
-//   nearest   rows u - lo exactly                      -> TU rows, slack 0
-//   canvas    j0 in {u-b-1, u-b}, j1 <= u-b+1, b = floor(off) -> TU+2 rows, slack 1
-//   npinterp  j = max{k: fl(off+k) <= u} may move +-1 more    -> TU+4 rows, slack 2
-template <int INTERP, int FORMULA>
-__host__ __device__ constexpr int box_slack() {
-    return INTERP == SSB_INTERP_NEAREST ? 0 : (FORMULA == SSB_FORMULA_CANVAS ? 1 : 2);
-}
-template <int INTERP, int FORMULA>
-__host__ __device__ constexpr int box_rows() {
-    return kTU + 2 * box_slack<INTERP, FORMULA>();
-}
-constexpr int kTX = 256;
-constexpr int kStages = 5;
+constexpr int kTX = 256;            // columns per tile (32 lanes x 8)
 constexpr int kQueue = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr uint32_t kRowBytes = kTX * 2;
-constexpr int kXzWords = 2 * 2 * kConsumerWarps * (kTX / 2);  // 2 buffers x 2 slices x warps x u16x2
+
+// Frame rows a tile needs (box height) and the slack above its first row:
+//   nearest   rows u - lo exactly                              -> TU rows, slack 0
+//   canvas    j0 in {u-b-1, u-b}, j1 <= u-b+1, b = floor(off)  -> TU+2 rows, slack 1
+//   npinterp  j = max{k: fl(off+k) <= u} may move +-1 more     -> TU+4 rows, slack 2
+template <int INTERP, int FORMULA>
+__host__ __device__ constexpr int box_slack() {
+    return INTERP == SSB_INTERP_NEAREST ? 0 : (FORMULA == SSB_FORMULA_CANVAS ? 1 : 2);
+}
+
+// Tile shape: 4 canvas rows per consumer warp (TU = 60, 5 stages) by default; projection-
+// only max mode (the live view, no volume to stream out) uses 8 rows (TU = 120, 3 stages),
+// amortising per-slice bookkeeping over twice the voxels.  Sum mode needs 8 u32
+// accumulators per row and always keeps 4 rows.
+template <int ROWS>
+struct Cfg {
+    static constexpr int kRows = ROWS;
+    static constexpr int kTU = kConsumerWarps * ROWS;
+    static constexpr int kBoxRows = kTU + 4;
+    static constexpr int kStages = ROWS >= 8 ? 3 : 5;
+    static constexpr int kXzBatch = ROWS >= 8 ? 1 : 2;  // max-mode slices per XZ barrier
+    static constexpr int kRowWords = (kTU + 31) / 32;   // 32-row groups the producer lanes cover
+    // XZ staging: max mode packs u16x2 (kTX/2 words per warp and slice); sum mode (ROWS 4) u32
+    static constexpr int kXzWords = ROWS >= 8 ? 2 * kXzBatch * kConsumerWarps * (kTX / 2)
+                                              : 2 * kConsumerWarps * kTX;
+    template <int INTERP, int FORMULA>
+    static constexpr int box_rows() {
+        return kTU + 2 * box_slack<INTERP, FORMULA>();
+    }
+};
+
 
 // Sampling parameters of one canvas row for one slice (written by the producer).
 // Rows outside the slice's span point both taps at a shared zero row with weights
@@ -83,14 +96,17 @@ struct Params {
     int32_t UT, XT, S, n_items, xy_accumulate;
 };
 
+template <int ROWS>
 struct Smem {
-    uint16_t box[kStages][kBoxRows][kTX];
+    using C = Cfg<ROWS>;
+    uint16_t box[C::kStages][C::kBoxRows][kTX];
     uint16_t zero_row[kTX];
-    RowP rows[kStages][kTU];
-    uint32_t hdr[kStages];  // bit 16: slice touches the tile (box loaded); bits 0..14: warps with live rows
-    alignas(16) uint32_t xz[kXzWords];
-    uint64_t full[kStages];
-    uint64_t empty[kStages];
+    RowP rows[C::kStages][C::kTU];
+    uint32_t hdr[C::kStages];  // bit 16: slice touches the tile; bits 0..14: warps with live rows;
+                               // bits 17..31: warps whose rows chain their taps
+    alignas(16) uint32_t xz[C::kXzWords];
+    uint64_t full[C::kStages];
+    uint64_t empty[C::kStages];
     uint64_t qfull[kQueue];
     uint64_t qempty[kQueue];
     int32_t queue[kQueue];
@@ -186,6 +202,18 @@ __device__ __forceinline__ uint32_t hmax8(const uint4 v) {
     return max(m & 0xFFFFu, m >> 16);
 }
 
+__device__ __forceinline__ uint32_t redux_max(uint32_t v) {
+    uint32_t r;
+    asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t redux_add(uint32_t v) {
+    uint32_t r;
+    asm volatile("redux.sync.add.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+
 // Row table entry of canvas row u for one slice (producer lanes).  Returns whether
 // the row is live (inside the window and the slice's span).
 template <int INTERP, int FORMULA>
@@ -219,57 +247,25 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     return true;
 }
 
-__device__ __forceinline__ uint32_t redux_max(uint32_t v) {
-    uint32_t r;
-    asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
-    return r;
-}
-
-__device__ __forceinline__ uint32_t redux_add(uint32_t v) {
-    uint32_t r;
-    asm volatile("redux.sync.add.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
-    return r;
-}
-
-// One consumer warp's 4 canvas rows of one slice: sample, store, fold into XY / XZ / YZ.
-// FULL: all 8 columns of every lane and all 4 rows are inside the output (no predicates).
-template <int INTERP, int FORMULA, bool kMax, bool FULL>
+// One consumer warp's ROWS canvas rows of one slice: sample, store, fold into XY / XZ / YZ.
+// FULL: all 8 columns of every lane and all rows are inside the output (no predicates).
+// With 4 rows the voxels of all rows are computed first and consumed afterwards (the tap
+// registers die before the accumulators are touched); with 8 rows each row is consumed
+// as soon as it is computed (keeps 8 rows of results out of the register file).
+template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS>
 __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off, const bool chained,
-                                          const bool want_yz, uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
-                                          uint4 (&acc_max)[kRows], uint32_t (&acc_sum)[kMax ? 1 : kRows][8],
-                                          uint4 &xz_max, uint32_t (&xz_sum)[8], uint32_t (&yzv)[kRows]) {
-    uint4 vs[kRows];
-    if (INTERP == SSB_INTERP_NEAREST) {
-#pragma unroll
-        for (int k = 0; k < kRows; ++k) vs[k] = lds128(rg[k].off_a + lane_off);
-    } else if (FORMULA == SSB_FORMULA_CANVAS && chained) {
-        // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
-        double prev[8];
-        to_biased8(lds128(rg[0].off_a + lane_off), prev);
-#pragma unroll
-        for (int k = 0; k < kRows; ++k) {
-            double cur[8];
-            to_biased8(lds128(rg[k].off_b + lane_off), cur);
-            vs[k] = lerp_biased8(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) prev[c] = cur[c];
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < kRows; ++k) {
-            const uint4 a = lds128(rg[k].off_a + lane_off);
-            const uint4 b = lds128(rg[k].off_b + lane_off);
-            vs[k] = voxels8<FORMULA>(a, b, rg[k]);
-        }
-    }
+                                          uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
+                                          uint4 (&acc_max)[ROWS], uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
+                                          uint4 &xz_max, uint32_t (&xz_sum)[8], uint32_t (&yzv)[ROWS]) {
+    constexpr bool kStream = ROWS > 4;
     const bool store = vrow != nullptr;
-#pragma unroll
-    for (int k = 0; k < kRows; ++k) {
-        const uint4 v = vs[k];
+    const bool chain = INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS && chained;
+    auto consume = [&](const int k, const uint4 v) {
         if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, v);
         if (kMax) {
             acc_max[k] = max_u16x8(acc_max[k], v);
-            if (want_yz) yzv[k] = redux_max(hmax8(v));
+            xz_max = max_u16x8(xz_max, v);
+            yzv[k] = redux_max(hmax8(v));
         } else {
             const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
             uint32_t rs = 0;
@@ -280,19 +276,46 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                 xz_sum[c] += e;
                 rs += e;
             }
-            if (want_yz) yzv[k] = redux_add(rs);
+            yzv[k] = redux_add(rs);
         }
+    };
+    uint4 vs[kStream ? 1 : ROWS];
+    double prev[8];
+    if (chain) to_biased8(lds128(rg[0].off_a + lane_off), prev);
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+        uint4 v;
+        if (INTERP == SSB_INTERP_NEAREST) {
+            v = lds128(rg[k].off_a + lane_off);
+        } else if (chain) {
+            // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
+            double cur[8];
+            to_biased8(lds128(rg[k].off_b + lane_off), cur);
+            v = lerp_biased8(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) prev[c] = cur[c];
+        } else {
+            v = voxels8<FORMULA>(lds128(rg[k].off_a + lane_off), lds128(rg[k].off_b + lane_off), rg[k]);
+        }
+        if (kStream) consume(k, v);
+        else vs[k] = v;
     }
-    if (kMax) xz_max = max_u16x8(max_u16x8(vs[0], vs[1]), max_u16x8(vs[2], vs[3]));
+    if (!kStream) {
+#pragma unroll
+        for (int k = 0; k < ROWS; ++k) consume(k, vs[k < (kStream ? 1 : ROWS) ? k : 0]);
+    }
 }
 
-template <int INTERP, int FORMULA, int REDUCE>
+template <int INTERP, int FORMULA, int REDUCE, int ROWS>
 __global__ void __launch_bounds__(kThreads, 1)
     deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
-    constexpr int kXzBatch = kMax ? 2 : 1;  // slices per XZ reduction (smem budget)
+    using C = Cfg<ROWS>;
+    constexpr int kTU = C::kTU;
+    constexpr int kStages = C::kStages;
+    constexpr int kXzBatch = kMax ? C::kXzBatch : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
+    Smem<ROWS> &sm = *reinterpret_cast<Smem<ROWS> *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
@@ -340,37 +363,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t box_r0 = tu0 - base - box_slack<INTERP, FORMULA>();
                 if (lane == 0) mbar_wait(&sm.empty[stage], sphase ^ 1);
                 __syncwarp();
-                uint32_t live_lo = 0, live_hi = 0;
+                uint32_t live[C::kRowWords];
+#pragma unroll
+                for (int j = 0; j < C::kRowWords; ++j) live[j] = 0;
                 if (hit) {
                     const uint32_t box_addr = smem_addr(&sm.box[stage][0][0]);
-                    bool l0, l1 = false;
-                    {
-                        const int r = lane;
-                        l0 = make_row<INTERP, FORMULA>(sm.rows[stage][r], tu0 + r, (int64_t)ut * kTU + r < p.u_count,
-                                                       lo, hi, off, p.h, box_r0, box_addr, zero_addr);
+#pragma unroll
+                    for (int j = 0; j < C::kRowWords; ++j) {
+                        const int r = lane + 32 * j;
+                        bool l = false;
+                        if (r < kTU)
+                            l = make_row<INTERP, FORMULA>(sm.rows[stage][r], tu0 + r,
+                                                          (int64_t)ut * kTU + r < p.u_count, lo, hi, off, p.h,
+                                                          box_r0, box_addr, zero_addr);
+                        live[j] = __ballot_sync(0xffffffffu, l);
                     }
-                    if (lane + 32 < kTU) {
-                        const int r = lane + 32;
-                        l1 = make_row<INTERP, FORMULA>(sm.rows[stage][r], tu0 + r, (int64_t)ut * kTU + r < p.u_count,
-                                                       lo, hi, off, p.h, box_r0, box_addr, zero_addr);
-                    }
-                    live_lo = __ballot_sync(0xffffffffu, l0);
-                    live_hi = __ballot_sync(0xffffffffu, l1);
                 }
                 __syncwarp();
-                // per consumer warp: any live row (bits 0..14); all four rows live with
-                // chained taps, off_b(k) == off_a(k+1), so tap rows can be converted once
-                // and reused by the next row (bits 17..31, canvas formula only)
-                const uint64_t live = (uint64_t)live_lo | ((uint64_t)live_hi << 32);
+                // per consumer warp: any live row (bits 0..14); all rows live with chained
+                // taps, off_b(k) == off_a(k+1), so tap rows are converted once and reused by
+                // the next row (bits 17..31, canvas formula only)
                 bool any = false, chained = false;
                 if (lane < kConsumerWarps) {
-                    const uint32_t bits = (uint32_t)(live >> (lane * kRows)) & ((1u << kRows) - 1);
+                    const int r0 = lane * ROWS;  // ROWS divides 32: a warp's rows share one word
+                    const uint32_t bits = (live[r0 / 32] >> (r0 % 32)) & ((1u << ROWS) - 1);
                     any = bits != 0;
-                    if (INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS && bits == (1u << kRows) - 1) {
-                        const RowP *g = &sm.rows[stage][lane * kRows];
+                    if (INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS && bits == (1u << ROWS) - 1) {
+                        const RowP *g = &sm.rows[stage][r0];
                         chained = true;
 #pragma unroll
-                        for (int k = 0; k + 1 < kRows; ++k) chained &= g[k].off_b == g[k + 1].off_a;
+                        for (int k = 0; k + 1 < ROWS; ++k) chained &= g[k].off_b == g[k + 1].off_a;
                     }
                 }
                 const uint32_t any_mask = __ballot_sync(0xffffffffu, any);
@@ -379,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) {
                     if (hit) {
-                        mbar_arrive_expect_tx(&sm.full[stage], box_rows<INTERP, FORMULA>() * kTX * 2);
+                        mbar_arrive_expect_tx(&sm.full[stage], C::template box_rows<INTERP, FORMULA>() * kRowBytes);
                         tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
                                     (int32_t)s, policy);
                     } else {
@@ -415,18 +437,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t s_begin = (int64_t)sc * p.chunk, s_end = min(p.n, s_begin + p.chunk);
         const int64_t x = (int64_t)xt * kTX + lane * 8;
         const bool col_ok = x < p.w;
-        const int64_t r0 = (int64_t)ut * kTU + warp * kRows;  // window row of k = 0
+        const int64_t r0 = (int64_t)ut * kTU + warp * ROWS;  // window row of k = 0
         const int64_t rows_left = p.u_count - r0;
-        const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= kRows ? kRows : (int)rows_left);
+        const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= ROWS ? ROWS : (int)rows_left);
         uint16_t *vrow = p.vol != nullptr ? p.vol + (size_t)s_begin * plane + (size_t)r0 * p.w + x : nullptr;
-        // warp-uniform fast path: every lane's 8 columns and all 4 rows inside the output
-        const bool fast = __all_sync(0xffffffffu, col_ok) && rows_ok == kRows;
-        const bool want_yz = p.yz != nullptr;
+        // warp-uniform fast path: every lane's 8 columns and all rows inside the output
+        const bool fast = __all_sync(0xffffffffu, col_ok) && rows_ok == ROWS;
 
-        uint4 acc_max[kRows];
-        uint32_t acc_sum[kMax ? 1 : kRows][8];
+        uint4 acc_max[ROWS];
+        uint32_t acc_sum[kMax ? 1 : ROWS][8];
 #pragma unroll
-        for (int k = 0; k < kRows; ++k) {
+        for (int k = 0; k < ROWS; ++k) {
             acc_max[k] = make_uint4(0, 0, 0, 0);
             if (!kMax)
 #pragma unroll
@@ -439,20 +460,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool live = (hdr >> 16) & (hdr >> warp) & 1u;
             uint4 xz_max = make_uint4(0, 0, 0, 0);
             uint32_t xz_sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            uint32_t yzv[kRows] = {0, 0, 0, 0};
+            uint32_t yzv[ROWS];
+#pragma unroll
+            for (int k = 0; k < ROWS; ++k) yzv[k] = 0;
             if (live) {
-                const RowP *rg = &sm.rows[stage][warp * kRows];
+                const RowP *rg = &sm.rows[stage][warp * ROWS];
                 const bool chained = (hdr >> (17 + warp)) & 1u;
                 if (fast)
-                    rows_pass<INTERP, FORMULA, kMax, true>(rg, lane_off, chained, want_yz, vrow, p.w, rows_ok, col_ok, acc_max,
-                                                          acc_sum, xz_max, xz_sum, yzv);
+                    rows_pass<INTERP, FORMULA, kMax, true, ROWS>(rg, lane_off, chained, vrow, p.w, rows_ok, col_ok,
+                                                                acc_max, acc_sum, xz_max, xz_sum, yzv);
                 else
-                    rows_pass<INTERP, FORMULA, kMax, false>(rg, lane_off, chained, want_yz, vrow, p.w, rows_ok, col_ok, acc_max,
-                                                           acc_sum, xz_max, xz_sum, yzv);
+                    rows_pass<INTERP, FORMULA, kMax, false, ROWS>(rg, lane_off, chained, vrow, p.w, rows_ok, col_ok,
+                                                                 acc_max, acc_sum, xz_max, xz_sum, yzv);
             } else if (vrow != nullptr && col_ok) {
                 const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
-                for (int k = 0; k < kRows; ++k)
+                for (int k = 0; k < ROWS; ++k)
                     if (k < rows_ok) stg_cs_v4(vrow + (size_t)k * p.w, z);
             }
             __syncwarp();
@@ -461,7 +484,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (vrow != nullptr) vrow += plane;
 
             if (p.yz != nullptr && lane < rows_ok) {
-                const uint32_t val = lane == 0 ? yzv[0] : lane == 1 ? yzv[1] : lane == 2 ? yzv[2] : yzv[3];
+                uint32_t val = yzv[0];
+#pragma unroll
+                for (int k = 1; k < ROWS; ++k)
+                    if (lane == k) val = yzv[k];
                 if (val != 0) red_u32<kMax>(p.yz + ((size_t)s * p.u_count + r0 + lane), val);
             }
 
@@ -469,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int g = (int)((s - s_begin) % kXzBatch);
                 const int buf = xz_batch & 1;
                 if (kMax) {
-                    uint32_t *dst = &sm.xz[((buf * 2 + g) * kConsumerWarps + warp) * (kTX / 2) + lane * 4];
+                    uint32_t *dst = &sm.xz[((buf * kXzBatch + g) * kConsumerWarps + warp) * (kTX / 2) + lane * 4];
                     *reinterpret_cast<uint4 *>(dst) = xz_max;
                 } else {
                     uint32_t *dst = &sm.xz[(buf * kConsumerWarps + warp) * kTX + lane * 8];
@@ -488,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             uint32_t red = 0;
 #pragma unroll
                             for (int w2 = 0; w2 < kConsumerWarps; ++w2)
-                                red = __vmaxu2(red, sm.xz[((buf * 2 + gg) * kConsumerWarps + w2) * (kTX / 2) + c2]);
+                                red = __vmaxu2(red, sm.xz[((buf * kXzBatch + gg) * kConsumerWarps + w2) * (kTX / 2) + c2]);
                             uint32_t *dst = p.xz + (size_t)(s0 + gg) * p.w + col;
                             if (red & 0xFFFFu) red_u32<true>(dst, red & 0xFFFFu);
                             if (red >> 16) red_u32<true>(dst + 1, red >> 16);
@@ -510,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.xy != nullptr && col_ok) {
             uint32_t *base = p.xy + (size_t)r0 * p.w + x;
 #pragma unroll
-            for (int k = 0; k < kRows; ++k) {
+            for (int k = 0; k < ROWS; ++k) {
                 if (k >= rows_ok) break;
                 uint32_t *dst = base + (size_t)k * p.w;
                 if (kMax) {
@@ -585,11 +611,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int INTERP, int FORMULA, int REDUCE>
+template <int INTERP, int FORMULA, int REDUCE, int ROWS>
 int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
-    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-    kern<<<grid, kThreads, sizeof(Smem), st>>>(map, prm);
+    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS>;
+    constexpr int smem = (int)sizeof(Smem<ROWS>);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<grid, kThreads, smem, st>>>(map, prm);
     return check_launch("deskew_tma_kernel");
 }
 
@@ -629,9 +656,13 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     CUtensorMap map;
     const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)d.n};
     const cuuint64_t strides[2] = {(cuuint64_t)row_stride_of(d) * 2, (cuuint64_t)frame_stride_of(d) * 2};
-    const int rows = d.interp == SSB_INTERP_NEAREST ? box_rows<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
-                     : d.formula == SSB_FORMULA_CANVAS ? box_rows<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>()
-                                                       : box_rows<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>();
+    const bool mx = d.reduce == SSB_REDUCE_MAX;
+    const bool tall = mx && vol == nullptr && env_i64("SSB_TALL_TILES", 1) != 0;
+    const int kTU = tall ? Cfg<8>::kTU : Cfg<4>::kTU;
+    const int slack = d.interp == SSB_INTERP_NEAREST ? box_slack<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
+                      : d.formula == SSB_FORMULA_CANVAS ? box_slack<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>()
+                                                        : box_slack<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>();
+    const int rows = kTU + 2 * slack;
     const cuuint32_t box[3] = {(cuuint32_t)kTX, (cuuint32_t)rows, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t *>(raw), dims,
@@ -655,7 +686,6 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     char *ws = static_cast<char *>(workspace);
     unsigned int *counters = reinterpret_cast<unsigned int *>(ws);
     ws += kCounterBytes;
-    const bool mx = d.reduce == SSB_REDUCE_MAX;
     const bool acc = (d.flags & SSB_FLAG_XY_ACCUMULATE) != 0;
     const size_t n_xy = (size_t)d.u_count * d.width, n_xz = (size_t)d.n * d.width, n_yz = (size_t)d.n * d.u_count;
     uint32_t *xy32 = nullptr, *xz32 = nullptr, *yz32 = nullptr;
@@ -700,14 +730,17 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     int rc;
     profile_begin(st);
     if (d.interp == SSB_INTERP_NEAREST)
-        rc = mx ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX>(map, prm, grid, st)
-                : launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM>(map, prm, grid, st);
+        rc = !mx ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4>(map, prm, grid, st)
+             : tall ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 8>(map, prm, grid, st)
+                    : launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 4>(map, prm, grid, st);
     else if (d.formula == SSB_FORMULA_CANVAS)
-        rc = mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX>(map, prm, grid, st)
-                : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM>(map, prm, grid, st);
+        rc = !mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4>(map, prm, grid, st)
+             : tall ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 8>(map, prm, grid, st)
+                    : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 4>(map, prm, grid, st);
     else
-        rc = mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_MAX>(map, prm, grid, st)
-                : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM>(map, prm, grid, st);
+        rc = !mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM, 4>(map, prm, grid, st)
+             : tall ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_MAX, 8>(map, prm, grid, st)
+                    : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_MAX, 4>(map, prm, grid, st);
     profile_end(st);
     count_launches(1);
     if (rc) return rc;
