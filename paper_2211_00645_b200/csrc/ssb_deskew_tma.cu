@@ -93,7 +93,8 @@ struct Params {
     unsigned int *counters;  // [0] next item (zeroed by the host before the launch)
     int64_t n, h, w, first, u_begin, u_count, chunk;
     double shear;
-    int32_t UT, XT, S, n_items, xy_accumulate;
+    int64_t n1, chunk2;  // phase split: slices [0, n1) in chunks of `chunk`, [n1, n) of `chunk2`
+    int32_t UT, XT, S, S2, n_items, xy_accumulate;
 };
 
 template <int ROWS>
@@ -112,14 +113,30 @@ struct Smem {
     int32_t queue[kQueue];
 };
 
-__device__ __forceinline__ void decode(int item, const Params &p, int &ut, int &xt, int &sc) {
-    sc = item % p.S;
-    const int rest = item / p.S;
+// Work item -> (u-tile, x-tile, slice range).  Two phases: every tile's first n1 slices in
+// big chunks, then the remaining slices in small chunks, so the dynamic scheduler ends on
+// short items (tail balance).  Within a phase u-tiles go centre-out (heaviest first).
+__device__ __forceinline__ void decode(int item, const Params &p, int &ut, int &xt, int64_t &s_begin,
+                                       int64_t &s_end) {
+    const int items1 = p.UT * p.XT * p.S;
+    int S = p.S, sc;
+    int64_t chunk = p.chunk, base = 0, stop = p.n1;
+    if (item >= items1) {
+        item -= items1;
+        S = p.S2;
+        chunk = p.chunk2;
+        base = p.n1;
+        stop = p.n;
+    }
+    sc = item % S;
+    const int rest = item / S;
     xt = rest % p.XT;
-    const int k = rest / p.XT;  // centre-out rank over u-tiles: heaviest tiles first
+    const int k = rest / p.XT;
     const int mid = (p.UT - 1) / 2;
     const int d = (k + 1) >> 1;
     ut = (k & 1) ? mid + d : mid - d;
+    s_begin = base + (int64_t)sc * chunk;
+    s_end = min(stop, s_begin + chunk);
 }
 
 __device__ __forceinline__ double biased(uint32_t v16) { return __hiloint2double(0x43300000, (int)v16); }
@@ -350,10 +367,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (++q == kQueue) { q = 0; qphase ^= 1; }
             if (done) break;
-            int ut, xt, sc;
-            decode(item, p, ut, xt, sc);
+            int ut, xt;
+            int64_t s_begin, s_end;
+            decode(item, p, ut, xt, s_begin, s_end);
             const int64_t tu0 = p.u_begin + (int64_t)ut * kTU;
-            const int64_t s_begin = (int64_t)sc * p.chunk, s_end = min(p.n, s_begin + p.chunk);
             for (int64_t s = s_begin; s < s_end; ++s) {
                 int64_t lo, hi;
                 double off;
@@ -432,9 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++q == kQueue) { q = 0; qphase ^= 1; }
         if (item < 0) break;
 
-        int ut, xt, sc;
-        decode(item, p, ut, xt, sc);
-        const int64_t s_begin = (int64_t)sc * p.chunk, s_end = min(p.n, s_begin + p.chunk);
+        int ut, xt;
+        int64_t s_begin, s_end;
+        decode(item, p, ut, xt, s_begin, s_end);
         const int64_t x = (int64_t)xt * kTX + lane * 8;
         const bool col_ok = x < p.w;
         const int64_t r0 = (int64_t)ut * kTU + warp * ROWS;  // window row of k = 0
@@ -676,11 +693,20 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     const int64_t UT = std::max<int64_t>(1, (d.u_count + kTU - 1) / kTU);
     const int64_t XT = std::max<int64_t>(1, (d.width + kTX - 1) / kTX);
     const int64_t tiles = UT * XT;
-    const int64_t want = env_i64("SSB_ITEMS_PER_CTA", 12) * sms;
-    int64_t S = std::max<int64_t>(1, std::min<int64_t>(d.n, (want + tiles - 1) / tiles));
-    const int64_t chunk = std::max<int64_t>(1, (d.n + S - 1) / S);
-    S = (d.n + chunk - 1) / chunk;
-    const int64_t items = tiles * S;
+    // phase 1: ~SSB_ITEMS_PER_CTA big items per CTA over the first SSB_BIG_PERCENT % of the
+    // slices; phase 2: the rest in ~SSB_TAIL_ITEMS_PER_CTA small items
+    auto split = [&](int64_t n_sl, int64_t per_cta, int64_t &S, int64_t &chunk) {
+        S = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n_sl, 1), (per_cta * sms + tiles - 1) / tiles));
+        chunk = std::max<int64_t>(1, (n_sl + S - 1) / S);
+        S = n_sl > 0 ? (n_sl + chunk - 1) / chunk : 0;
+    };
+    const int64_t big_pct = std::min<int64_t>(100, std::max<int64_t>(0, env_i64("SSB_BIG_PERCENT", 85)));
+    int64_t n1 = d.n * big_pct / 100;
+    if (n1 < 1) n1 = d.n;
+    int64_t S, chunk, S2, chunk2;
+    split(n1, env_i64("SSB_ITEMS_PER_CTA", 2), S, chunk);
+    split(d.n - n1, env_i64("SSB_TAIL_ITEMS_PER_CTA", 6), S2, chunk2);
+    const int64_t items = tiles * (S + S2);
     if (items > INT32_MAX / 2) return fail(SSB_ERR_CAPACITY, "too many tiles");
 
     char *ws = static_cast<char *>(workspace);
@@ -719,6 +745,9 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     prm.u_begin = d.u_begin;
     prm.u_count = d.u_count;
     prm.chunk = chunk;
+    prm.n1 = n1;
+    prm.chunk2 = chunk2;
+    prm.S2 = (int32_t)S2;
     prm.shear = d.shear_px;
     prm.UT = (int32_t)UT;
     prm.XT = (int32_t)XT;
