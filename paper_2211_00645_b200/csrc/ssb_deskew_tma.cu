@@ -5,17 +5,18 @@
 // ss/geometry.py:236-255 spans), organised for B200:
 //
 //  * one persistent CTA per SM: 15 consumer warps + 1 producer warp;
-//  * the producer pulls work items from a global atomic counter (tiles ordered
-//    centre-out over the canvas rows, i.e. heaviest first), and for every slice
-//    that touches the tile issues one 3-D TMA box load (256 columns x TU+4 frame
-//    rows) into a 4-stage shared-memory ring guarded by full/empty mbarriers; its
-//    lanes also derive the per-row sampling parameters (fp64, once per row per
-//    slice instead of once per thread);
-//  * consumer warp w owns 4 canvas rows, lane l 8 columns: it reads the two frame
-//    rows of each canvas row from shared memory (conflict-free 512 B rows),
-//    evaluates 8 voxels with the exact fp64 expression, streams them to the volume
-//    with st.global.cs, and folds them into the XY (registers), YZ (REDUX) and
-//    XZ (shared memory, named barrier) reductions;
+//  * the producer pulls work items (u-tile x 256-column x-tile x slice chunk) from a
+//    global atomic counter -- big chunks first, a tail of short chunks last, u-tiles
+//    centre-out (heaviest first) -- and for every slice that touches the tile issues
+//    one 3-D TMA box load (256 columns x TU+2*slack frame rows, OOB zero-filled) into a
+//    5-stage (3 for 8-row tiles) shared-memory ring guarded by full/empty mbarriers;
+//    its lanes also derive the per-row sampling table (fp64, once per row per slice);
+//  * consumer warp w owns 4 (or 8) canvas rows, lane l 8 columns: it reads the two
+//    taps of each canvas row from shared memory (conflict-free 512 B rows; chained
+//    rows reuse the converted tap row), evaluates 8 voxels with the exact fp64
+//    expression, streams them to the volume with st.global.cs, and folds them into the
+//    XY (registers), YZ (REDUX) and XZ (shared memory, named barrier) reductions, which
+//    land in u32 scratch through L2 reductions (red.global.max/add);
 //  * int->double conversion is folded into the products: fma(w, 2^52 + a,
 //    -w*2^52) == fl(w*a) exactly (one rounding), so a voxel costs 2 DFMA + 2 DADD.
 #include <algorithm>
@@ -235,7 +236,8 @@ __device__ __forceinline__ uint32_t redux_add(uint32_t v) {
 // the row is live (inside the window and the slice's span).
 template <int INTERP, int FORMULA>
 __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int64_t lo, int64_t hi, double off,
-                                         int64_t h, int64_t box_r0, uint32_t box_addr, uint32_t zero_addr) {
+                                         int64_t h, int64_t box_r0, int64_t box_rows, uint32_t box_addr,
+                                         uint32_t zero_addr) {
     o.c0 = 1.0;
     o.c1 = 0.0;
     o.n0 = -kTwo52;
@@ -249,6 +251,9 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     }
     if (!in_window || u < lo || u > hi) return false;
     const RowParam rp = row_param<INTERP, FORMULA>(u, lo, off, h);
+    // the box covers [box_r0, box_r0 + TU + 2*slack): a tap outside it would read another
+    // stage's data -- fail loudly instead (cheap: once per row per slice, producer warp only)
+    if (rp.j0 < box_r0 || rp.j1 < box_r0 || rp.j0 - box_r0 >= box_rows || rp.j1 - box_r0 >= box_rows) __trap();
     o.off_a = box_addr + (uint32_t)(rp.j0 - box_r0) * kRowBytes;
     o.off_b = box_addr + (uint32_t)(rp.j1 - box_r0) * kRowBytes;
     if (rp.kind >= 2) {
@@ -392,7 +397,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (r < kTU)
                             l = make_row<INTERP, FORMULA>(sm.rows[stage][r], tu0 + r,
                                                           (int64_t)ut * kTU + r < p.u_count, lo, hi, off, p.h,
-                                                          box_r0, box_addr, zero_addr);
+                                                          box_r0, C::template box_rows<INTERP, FORMULA>(), box_addr,
+                                                          zero_addr);
                         live[j] = __ballot_sync(0xffffffffu, l);
                     }
                 }
