@@ -191,7 +191,22 @@ __device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
     }
 }
 
-// canvas lerp of 8 voxels from biased taps: rint(fl(fl(w0*a) + fl(f*b)))
+// canvas lerp of 8 voxels from biased taps: rint(fl(fl(w0*a) + fl(f*b))) as 8 u32 values
+__device__ __forceinline__ void lerp_biased8_raw(const double (&a)[8], const double (&b)[8], const double c0,
+                                                 const double c1, const double n0, const double n1,
+                                                 uint32_t (&r)[8]) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        r[c] = (uint32_t)__double2loint(
+            __dadd_rn(__dadd_rn(__fma_rn(c0, a[c], n0), __fma_rn(c1, b[c], n1)), kRintMagic));
+}
+
+__device__ __forceinline__ uint4 pack8(const uint32_t (&r)[8]) {
+    return make_uint4(__byte_perm(r[0], r[1], 0x5410), __byte_perm(r[2], r[3], 0x5410),
+                      __byte_perm(r[4], r[5], 0x5410), __byte_perm(r[6], r[7], 0x5410));
+}
+
+// ... and packed 8 x uint16
 __device__ __forceinline__ uint4 lerp_biased8(const double (&a)[8], const double (&b)[8], const double c0,
                                               const double c1, const double n0, const double n1) {
     uint32_t r[8];
@@ -274,12 +289,12 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
 // With 4 rows the voxels of all rows are computed first and consumed afterwards (the tap
 // registers die before the accumulators are touched); with 8 rows each row is consumed
 // as soon as it is computed (keeps 8 rows of results out of the register file).
-template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS>
+template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE>
 __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off, const bool chained,
                                           uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
                                           uint4 (&acc_max)[ROWS], uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
                                           uint4 &xz_max, uint32_t (&xz_sum)[8], uint32_t (&yzv)[ROWS]) {
-    constexpr bool kStream = ROWS > 4;
+    constexpr bool kStream = ROWS > 4 || (!kMax && !SIDE);
     const bool store = vrow != nullptr;
     const bool chain = INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS && chained;
     auto consume = [&](const int k, const uint4 v) {
@@ -295,10 +310,12 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
             for (int c = 0; c < 8; ++c) {
                 const uint32_t e = (w4[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
                 acc_sum[k][c] += e;
-                xz_sum[c] += e;
-                rs += e;
+                if (SIDE) {  // XZ / YZ requested (compile-time: XY-only sums skip this work)
+                    xz_sum[c] += e;
+                    rs += e;
+                }
             }
-            yzv[k] = redux_add(rs);
+            if (SIDE) yzv[k] = redux_add(rs);
         }
     };
     uint4 vs[kStream ? 1 : ROWS];
@@ -313,6 +330,25 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
             // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
             double cur[8];
             to_biased8(lds128(rg[k].off_b + lane_off), cur);
+            if (!kMax && kStream) {
+                // sums take the rounded voxels straight from the rint trick (no unpacking)
+                uint32_t r[8];
+                lerp_biased8_raw(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1, r);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) prev[c] = cur[c];
+                if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, pack8(r));
+                uint32_t rs = 0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    acc_sum[k][c] += r[c];
+                    if (SIDE) {
+                        xz_sum[c] += r[c];
+                        rs += r[c];
+                    }
+                }
+                if (SIDE) yzv[k] = redux_add(rs);
+                continue;
+            }
             v = lerp_biased8(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1);
 #pragma unroll
             for (int c = 0; c < 8; ++c) prev[c] = cur[c];
@@ -328,7 +364,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     }
 }
 
-template <int INTERP, int FORMULA, int REDUCE, int ROWS>
+template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE>
 __global__ void __launch_bounds__(kThreads, 1)
     deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
@@ -490,10 +526,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const RowP *rg = &sm.rows[stage][warp * ROWS];
                 const bool chained = (hdr >> (17 + warp)) & 1u;
                 if (fast)
-                    rows_pass<INTERP, FORMULA, kMax, true, ROWS>(rg, lane_off, chained, vrow, p.w, rows_ok, col_ok,
+                    rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE>(rg, lane_off, chained, vrow, p.w, rows_ok, col_ok,
                                                                 acc_max, acc_sum, xz_max, xz_sum, yzv);
                 else
-                    rows_pass<INTERP, FORMULA, kMax, false, ROWS>(rg, lane_off, chained, vrow, p.w, rows_ok, col_ok,
+                    rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE>(rg, lane_off, chained, vrow, p.w, rows_ok, col_ok,
                                                                  acc_max, acc_sum, xz_max, xz_sum, yzv);
             } else if (vrow != nullptr && col_ok) {
                 const uint4 z = make_uint4(0, 0, 0, 0);
@@ -634,9 +670,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int INTERP, int FORMULA, int REDUCE, int ROWS>
+template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE = true>
 int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
-    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS>;
+    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE>;
     constexpr int smem = (int)sizeof(Smem<ROWS>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<grid, kThreads, smem, st>>>(map, prm);
@@ -680,7 +716,8 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)d.n};
     const cuuint64_t strides[2] = {(cuuint64_t)row_stride_of(d) * 2, (cuuint64_t)frame_stride_of(d) * 2};
     const bool mx = d.reduce == SSB_REDUCE_MAX;
-    const bool tall = mx && vol == nullptr && env_i64("SSB_TALL_TILES", 1) != 0;
+    const bool side = xz != nullptr || yz != nullptr;
+    const bool tall = vol == nullptr && env_i64("SSB_TALL_TILES", 1) != 0 && (mx || !side);
     const int kTU = tall ? Cfg<8>::kTU : Cfg<4>::kTU;
     const int slack = d.interp == SSB_INTERP_NEAREST ? box_slack<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
                       : d.formula == SSB_FORMULA_CANVAS ? box_slack<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>()
@@ -764,7 +801,19 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
 
     int rc;
     profile_begin(st);
-    if (d.interp == SSB_INTERP_NEAREST)
+    // one place decides the instantiation, consistent with the tile height planned above
+    if (!mx && !side) {
+        // XY-only sums (the long-scan live view): no XZ / YZ work
+        if (d.interp == SSB_INTERP_NEAREST)
+            rc = tall ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 8, false>(map, prm, grid, st)
+                      : launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
+        else if (d.formula == SSB_FORMULA_CANVAS)
+            rc = tall ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 8, false>(map, prm, grid, st)
+                      : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
+        else
+            rc = tall ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM, 8, false>(map, prm, grid, st)
+                      : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
+    } else if (d.interp == SSB_INTERP_NEAREST)
         rc = !mx ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4>(map, prm, grid, st)
              : tall ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 8>(map, prm, grid, st)
                     : launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 4>(map, prm, grid, st);
