@@ -467,3 +467,24 @@ def test_rolling_incremental_matches_full_remax_with_ties(seed):
         canvas[lo:hi + 1], contrib[lo:hi + 1] = band, cb
         np.testing.assert_array_equal(c.max_pixels, canvas)
         np.testing.assert_array_equal(c.contributor, contrib)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("tall", ["1", "0"])
+def test_projection_only_variants(seed, tall, monkeypatch):
+    """Projection-only launches pick other kernel instantiations: 8-row tiles for max,
+    XY-only sums without XZ/YZ work.  Every combination against the C oracle."""
+    monkeypatch.setenv("SSB_TALL_TILES", tall)
+    rng = np.random.default_rng(900 + seed)
+    n, h, w = int(rng.integers(1, 60)), int(rng.integers(1, 300)), 8 * int(rng.integers(1, 70))
+    s = float(rng.choice([rng.uniform(0, 2.2), 0.7071067811865476, 1.0, 0.5]))
+    st = rng.integers(0, 65536, (n, h, w)).astype(np.uint16)
+    for interp in ("linear", "nearest"):
+        for formula in (("canvas", "npinterp") if interp == "linear" else ("canvas",)):
+            for reduce in ("max", "sum"):
+                for axes in ((0,), (0, 1, 2), (1,), (2,)):
+                    _, want = C.deskew(st, s, interp, formula, want_volume=False, axes=axes, reduce=reduce)
+                    vol, pr = run(st, s, interp, formula, reduce, write_volume=False, projection_axes=axes)
+                    assert vol is None
+                    for ax in axes:
+                        np.testing.assert_array_equal(pr[ax], want[ax], err_msg=f"{interp} {formula} {reduce} {axes}")
