@@ -289,14 +289,14 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
 // With 4 rows the voxels of all rows are computed first and consumed afterwards (the tap
 // registers die before the accumulators are touched); with 8 rows each row is consumed
 // as soon as it is computed (keeps 8 rows of results out of the register file).
-template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE>
-__device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off, const bool chained,
+template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN>
+__device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off,
                                           uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
                                           uint4 (&acc_max)[ROWS], uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
                                           uint4 &xz_max, uint32_t (&xz_sum)[8], uint32_t (&yzv)[ROWS]) {
     constexpr bool kStream = ROWS > 4 || (!kMax && !SIDE);
     const bool store = vrow != nullptr;
-    const bool chain = INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS && chained;
+    constexpr bool chain = CHAIN && INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS;
     auto consume = [&](const int k, const uint4 v) {
         if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, v);
         if (kMax) {
@@ -502,6 +502,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint16_t *vrow = p.vol != nullptr ? p.vol + (size_t)s_begin * plane + (size_t)r0 * p.w + x : nullptr;
         // warp-uniform fast path: every lane's 8 columns and all rows inside the output
         const bool fast = __all_sync(0xffffffffu, col_ok) && rows_ok == ROWS;
+        uint32_t *yzp = p.yz != nullptr ? p.yz + (size_t)s_begin * p.u_count + r0 + lane : nullptr;
+        const bool has_xz = p.xz != nullptr;
+        int g = 0;  // slice within the current XZ batch
 
         uint4 acc_max[ROWS];
         uint32_t acc_sum[kMax ? 1 : ROWS][8];
@@ -513,7 +516,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < 8; ++c) acc_sum[k][c] = 0;
         }
 
-        for (int64_t s = s_begin; s < s_end; ++s) {
+        const int ns = (int)(s_end - s_begin);
+        for (int si = 0; si < ns; ++si) {
             mbar_wait(&sm.full[stage], sphase);
             const uint32_t hdr = sm.hdr[stage];
             const bool live = (hdr >> 16) & (hdr >> warp) & 1u;
@@ -525,12 +529,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (live) {
                 const RowP *rg = &sm.rows[stage][warp * ROWS];
                 const bool chained = (hdr >> (17 + warp)) & 1u;
-                if (fast)
-                    rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE>(rg, lane_off, chained, vrow, p.w, rows_ok, col_ok,
-                                                                acc_max, acc_sum, xz_max, xz_sum, yzv);
-                else
-                    rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE>(rg, lane_off, chained, vrow, p.w, rows_ok, col_ok,
-                                                                 acc_max, acc_sum, xz_max, xz_sum, yzv);
+                // four specialisations so the row loop has no per-row branches
+                if (fast) {
+                    if (chained)
+                        rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE, true>(rg, lane_off, vrow, p.w, rows_ok,
+                                                                                col_ok, acc_max, acc_sum, xz_max,
+                                                                                xz_sum, yzv);
+                    else
+                        rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE, false>(rg, lane_off, vrow, p.w, rows_ok,
+                                                                                 col_ok, acc_max, acc_sum, xz_max,
+                                                                                 xz_sum, yzv);
+                } else {
+                    if (chained)
+                        rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE, true>(rg, lane_off, vrow, p.w, rows_ok,
+                                                                                 col_ok, acc_max, acc_sum, xz_max,
+                                                                                 xz_sum, yzv);
+                    else
+                        rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE, false>(rg, lane_off, vrow, p.w, rows_ok,
+                                                                                  col_ok, acc_max, acc_sum, xz_max,
+                                                                                  xz_sum, yzv);
+                }
             } else if (vrow != nullptr && col_ok) {
                 const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -542,16 +560,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++stage == kStages) { stage = 0; sphase ^= 1; }
             if (vrow != nullptr) vrow += plane;
 
-            if (p.yz != nullptr && lane < rows_ok) {
-                uint32_t val = yzv[0];
+            if (yzp != nullptr) {
+                if (lane < rows_ok) {
+                    uint32_t val = yzv[0];
 #pragma unroll
-                for (int k = 1; k < ROWS; ++k)
-                    if (lane == k) val = yzv[k];
-                if (val != 0) red_u32<kMax>(p.yz + ((size_t)s * p.u_count + r0 + lane), val);
+                    for (int k = 1; k < ROWS; ++k)
+                        if (lane == k) val = yzv[k];
+                    if (val != 0) red_u32<kMax>(yzp, val);
+                }
+                yzp += p.u_count;
             }
 
-            if (p.xz != nullptr) {
-                const int g = (int)((s - s_begin) % kXzBatch);
+            if (has_xz) {
                 const int buf = xz_batch & 1;
                 if (kMax) {
                     uint32_t *dst = &sm.xz[((buf * kXzBatch + g) * kConsumerWarps + warp) * (kTX / 2) + lane * 4];
@@ -561,10 +581,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *reinterpret_cast<uint4 *>(dst) = make_uint4(xz_sum[0], xz_sum[1], xz_sum[2], xz_sum[3]);
                     *reinterpret_cast<uint4 *>(dst + 4) = make_uint4(xz_sum[4], xz_sum[5], xz_sum[6], xz_sum[7]);
                 }
-                const bool flush = g == kXzBatch - 1 || s + 1 == s_end;
-                if (flush) {
+                if (g == kXzBatch - 1 || si + 1 == ns) {
                     named_bar_sync(1, kConsumerThreads);
-                    const int64_t s0 = s - g;  // first slice of this batch
+                    const int64_t s0 = s_begin + si - g;  // first slice of this batch
                     if (kMax) {
                         // thread -> (slice of batch, word of 2 columns)
                         const int gg = tid / (kTX / 2), c2 = tid % (kTX / 2);
@@ -588,6 +607,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     ++xz_batch;
+                    g = 0;
+                } else {
+                    ++g;
                 }
             }
         }
