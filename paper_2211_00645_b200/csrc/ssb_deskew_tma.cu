@@ -301,8 +301,10 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, v);
         if (kMax) {
             acc_max[k] = max_u16x8(acc_max[k], v);
-            xz_max = max_u16x8(xz_max, v);
-            yzv[k] = redux_max(hmax8(v));
+            if (SIDE) {  // XZ / YZ requested (compile-time: XY-only views skip this work)
+                xz_max = max_u16x8(xz_max, v);
+                yzv[k] = redux_max(hmax8(v));
+            }
         } else {
             const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
             uint32_t rs = 0;
@@ -701,6 +703,23 @@ int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t
     return check_launch("deskew_tma_kernel");
 }
 
+// Kernel instantiation for (reduce, tile height, side projections requested):
+//   max:  {4, 8 rows} x {with, without XZ/YZ}      sum: 4 rows with XZ/YZ, {4, 8} rows XY-only
+template <int INTERP, int FORMULA>
+int launch_variant(bool mx, bool tall, bool side, const CUtensorMap &map, const Params &prm, int grid,
+                   cudaStream_t st) {
+    if (mx) {
+        if (side)
+            return tall ? launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 8, true>(map, prm, grid, st)
+                        : launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, true>(map, prm, grid, st);
+        return tall ? launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 8, false>(map, prm, grid, st)
+                    : launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, false>(map, prm, grid, st);
+    }
+    if (side) return launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, true>(map, prm, grid, st);
+    return tall ? launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 8, false>(map, prm, grid, st)
+                : launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
+}
+
 }  // namespace tma_path
 
 bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol, const void *xy) {
@@ -824,29 +843,12 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     int rc;
     profile_begin(st);
     // one place decides the instantiation, consistent with the tile height planned above
-    if (!mx && !side) {
-        // XY-only sums (the long-scan live view): no XZ / YZ work
-        if (d.interp == SSB_INTERP_NEAREST)
-            rc = tall ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 8, false>(map, prm, grid, st)
-                      : launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
-        else if (d.formula == SSB_FORMULA_CANVAS)
-            rc = tall ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 8, false>(map, prm, grid, st)
-                      : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
-        else
-            rc = tall ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM, 8, false>(map, prm, grid, st)
-                      : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
-    } else if (d.interp == SSB_INTERP_NEAREST)
-        rc = !mx ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4>(map, prm, grid, st)
-             : tall ? launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 8>(map, prm, grid, st)
-                    : launch_one<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 4>(map, prm, grid, st);
+    if (d.interp == SSB_INTERP_NEAREST)
+        rc = launch_variant<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>(mx, tall, side, map, prm, grid, st);
     else if (d.formula == SSB_FORMULA_CANVAS)
-        rc = !mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_SUM, 4>(map, prm, grid, st)
-             : tall ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 8>(map, prm, grid, st)
-                    : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS, SSB_REDUCE_MAX, 4>(map, prm, grid, st);
+        rc = launch_variant<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>(mx, tall, side, map, prm, grid, st);
     else
-        rc = !mx ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_SUM, 4>(map, prm, grid, st)
-             : tall ? launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_MAX, 8>(map, prm, grid, st)
-                    : launch_one<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP, SSB_REDUCE_MAX, 4>(map, prm, grid, st);
+        rc = launch_variant<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>(mx, tall, side, map, prm, grid, st);
     profile_end(st);
     count_launches(1);
     if (rc) return rc;

@@ -18,19 +18,22 @@ ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--hw", type=int, default=2048)
 ap.add_argument("--no-volume", action="store_true")
 ap.add_argument("--formula", default="canvas")
+ap.add_argument("--axes", default="0,1,2")
 a = ap.parse_args()
+axes = tuple(int(v) for v in a.axes.split(","))
 s = math.cos(math.radians(30.0))
 g = torch.Generator(device="cuda").manual_seed(1234)
 raw = torch.randint(0, 4096, (a.n, a.hw, a.hw), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
 res = None
 for _ in range(a.iters):
-    res = deskew_device(raw, s, a.interp, reduce=a.reduce, formula=a.formula, write_volume=not a.no_volume)
+    res = deskew_device(raw, s, a.interp, reduce=a.reduce, formula=a.formula, write_volume=not a.no_volume,
+                        projection_axes=axes)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(a.iters):
     deskew_device(raw, s, a.interp, reduce=a.reduce, formula=a.formula, write_volume=not a.no_volume,
-                  volume=res.volume, projections=res.projections)
+                  volume=res.volume, projections=res.projections, projection_axes=axes)
 e1.record()
 torch.cuda.synchronize()
-print(f"{a.interp} {a.reduce} vol={not a.no_volume}: {e0.elapsed_time(e1) / a.iters:.3f} ms/call")
+print(f"{a.interp} {a.reduce} vol={not a.no_volume} axes={a.axes}: {e0.elapsed_time(e1) / a.iters:.3f} ms/call")
