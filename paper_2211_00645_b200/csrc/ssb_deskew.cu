@@ -350,7 +350,10 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
         return check_launch("ssb_deskew(empty)");
     }
     if (raw == nullptr) return fail(SSB_ERR_PARAM, "raw frames pointer is null");
-    const bool use_tma = env_int("SSB_DISABLE_TMA", 0) == 0 && tma_eligible(*d, raw, vol, xy);
+    // a handful of frames folded into XY only (ProjectionCanvas.place, ss/pipeline.py:316-323) is
+    // one small launch of the tiled kernel: no scratch reset, no finalize pass
+    const bool tiny = d->n <= 2 && xz == nullptr && yz == nullptr;
+    const bool use_tma = env_int("SSB_DISABLE_TMA", 0) == 0 && !tiny && tma_eligible(*d, raw, vol, xy);
     if (use_tma) return launch_deskew_tma(*d, raw, vol, xy, xz, yz, workspace, workspace_bytes, st);
 
     const Plan pl = make_plan(*d, xy != nullptr, xz != nullptr, yz != nullptr, tiled_rows(*d), false);

@@ -158,9 +158,17 @@ class ProjectionCanvas:
         return all(rf is None for rf in self._ring)
 
     def _upload(self, pixels: np.ndarray) -> torch.Tensor:
+        """Frame -> device on the canvas stream; asynchronous when the frame already lives in
+        page-locked memory (e.g. a view of ``ingest.load_stack`` / ``stream.pinned_stack``)."""
         host = torch.from_numpy(np.ascontiguousarray(pixels))
+        pinned = host.is_pinned()
         with torch.cuda.stream(self.stream):
-            return host.to(self._device, non_blocking=False).unsqueeze(0)
+            dev = host.to(self._device, non_blocking=pinned).unsqueeze(0)
+        if pinned:
+            # RawFrame pixels are immutable (ss/pipeline.py:37-39), so the copy may still be
+            # reading them after place() returns; hold a reference until the next upload
+            self._pending_upload = host
+        return dev
 
     @property
     def max_pixels(self) -> np.ndarray:
