@@ -488,3 +488,34 @@ def test_projection_only_variants(seed, tall, monkeypatch):
                     assert vol is None
                     for ax in axes:
                         np.testing.assert_array_equal(pr[ax], want[ax], err_msg=f"{interp} {formula} {reduce} {axes}")
+
+
+def test_empty_and_degenerate_inputs():
+    d = dev()
+    empty = torch.empty((0, 16, 32), dtype=torch.uint16, device=d)
+    res = deskew_device(empty, 1.0, "linear", canvas_rows=16, projection_axes=(0,))
+    torch.cuda.synchronize()
+    assert res.projections[0].shape == (16, 32)
+    assert int(res.projections[0].to(torch.int32).abs().sum()) == 0
+    # zero-width canvas window: nothing to do, no error
+    raw = torch.ones((3, 4, 8), dtype=torch.uint16, device=d)
+    res = deskew_device(raw, 1.0, "linear", u_begin=2, u_count=0, projection_axes=(0,), write_volume=False)
+    torch.cuda.synchronize()
+    assert res.projections[0].shape == (0, 8)
+    with pytest.raises(ParameterError):
+        deskew_device(raw, -0.5, "linear")
+    with pytest.raises(ParameterError):
+        deskew_device(raw.to(torch.int16), 1.0, "linear")
+    with pytest.raises(ParameterError, match="empty"):
+        ph.reference_deskew([], geom(), 1.0)
+
+
+def test_deskew_volume_device_api():
+    rng = np.random.default_rng(12)
+    st = rng.integers(0, 65536, (10, 24, 64)).astype(np.uint16)
+    res = deskew_volume(torch.from_numpy(st).to(dev()), geom(n=10, w=64, h=24), 0.73, "nearest",
+                        projection_axes=(1,), reduce="sum")
+    assert isinstance(res.volume, torch.Tensor) and res.volume.is_cuda
+    want_vol, want = C.deskew(st, 0.73, "nearest", reduce="sum")
+    np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
+    np.testing.assert_array_equal(res.xz.cpu().numpy(), want[1])
