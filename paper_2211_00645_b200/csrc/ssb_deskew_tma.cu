@@ -181,6 +181,26 @@ __device__ __forceinline__ uint4 voxels8(const uint4 a, const uint4 b, const Row
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
+// Tap conversion for the chained canvas path.  SSB_NATIVE_CVT: native I2F.F64 conversions (one
+// conversion-pipe op per tap value, measured 16/clk/SM on B200 -- the path needs ~6.5/clk at
+// roofline) and plain DMUL products, fl(w*a).  With SSB_MAGIC_CVT: the 2^52 trick (integer
+// extract + constant high word, DFMA with -w*2^52).  Both round exactly like numpy; measured
+// on B200 the magic form is equal with a volume and 2-3 % faster projection-only, so it is
+// the default.
+#if !defined(SSB_MAGIC_CVT) && !defined(SSB_NATIVE_CVT)
+#define SSB_MAGIC_CVT
+#endif
+#ifdef SSB_NATIVE_CVT
+__device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
+    const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        o[2 * q] = __uint2double_rn(w4[q] & 0xFFFFu);
+        o[2 * q + 1] = __uint2double_rn(w4[q] >> 16);
+    }
+}
+__device__ __forceinline__ double tap_prod(double c, double a, double /*n*/) { return __dmul_rn(c, a); }
+#else
 // 8 packed uint16 -> 8 doubles 2^52 + v (exact; one integer op + the constant high word each)
 __device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
     const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
@@ -190,15 +210,17 @@ __device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
         o[2 * q + 1] = biased(w4[q] >> 16);
     }
 }
+__device__ __forceinline__ double tap_prod(double c, double a, double n) { return __fma_rn(c, a, n); }
+#endif
 
-// canvas lerp of 8 voxels from biased taps: rint(fl(fl(w0*a) + fl(f*b))) as 8 u32 values
+// canvas lerp of 8 voxels from converted taps: rint(fl(fl(w0*a) + fl(f*b))) as 8 u32 values
 __device__ __forceinline__ void lerp_biased8_raw(const double (&a)[8], const double (&b)[8], const double c0,
                                                  const double c1, const double n0, const double n1,
                                                  uint32_t (&r)[8]) {
 #pragma unroll
     for (int c = 0; c < 8; ++c)
         r[c] = (uint32_t)__double2loint(
-            __dadd_rn(__dadd_rn(__fma_rn(c0, a[c], n0), __fma_rn(c1, b[c], n1)), kRintMagic));
+            __dadd_rn(__dadd_rn(tap_prod(c0, a[c], n0), tap_prod(c1, b[c], n1)), kRintMagic));
 }
 
 __device__ __forceinline__ uint4 pack8(const uint32_t (&r)[8]) {
@@ -210,12 +232,8 @@ __device__ __forceinline__ uint4 pack8(const uint32_t (&r)[8]) {
 __device__ __forceinline__ uint4 lerp_biased8(const double (&a)[8], const double (&b)[8], const double c0,
                                               const double c1, const double n0, const double n1) {
     uint32_t r[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-        r[c] = (uint32_t)__double2loint(
-            __dadd_rn(__dadd_rn(__fma_rn(c0, a[c], n0), __fma_rn(c1, b[c], n1)), kRintMagic));
-    return make_uint4(__byte_perm(r[0], r[1], 0x5410), __byte_perm(r[2], r[3], 0x5410),
-                      __byte_perm(r[4], r[5], 0x5410), __byte_perm(r[6], r[7], 0x5410));
+    lerp_biased8_raw(a, b, c0, c1, n0, n1, r);
+    return pack8(r);
 }
 
 template <bool kMax>
@@ -421,7 +439,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool hit = !(hi < tu0 || lo > tu0 + kTU - 1);
                 const int64_t base = INTERP == SSB_INTERP_NEAREST ? lo : (int64_t)floor(off);
                 const int64_t box_r0 = tu0 - base - box_slack<INTERP, FORMULA>();
-                if (lane == 0) mbar_wait(&sm.empty[stage], sphase ^ 1);
+                // the box load goes out as soon as the stage is free; the row table is built
+                // while it is in flight (full completes on the bytes + all 32 lane arrivals)
+                if (lane == 0) {
+                    mbar_wait(&sm.empty[stage], sphase ^ 1);
+                    if (hit) {
+                        mbar_expect_tx(&sm.full[stage], C::template box_rows<INTERP, FORMULA>() * kRowBytes);
+                        tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
+                                    (int32_t)s, policy);
+                    }
+                }
                 __syncwarp();
                 uint32_t live[C::kRowWords];
 #pragma unroll
@@ -460,17 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t chain_mask = __ballot_sync(0xffffffffu, chained);
                 if (lane == 0) sm.hdr[stage] = any_mask | (hit ? (1u << 16) : 0u) | (chain_mask << 17);
                 __syncwarp();
-                if (lane == 0) {
-                    if (hit) {
-                        mbar_arrive_expect_tx(&sm.full[stage], C::template box_rows<INTERP, FORMULA>() * kRowBytes);
-                        tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
-                                    (int32_t)s, policy);
-                    } else {
-                        mbar_arrive(&sm.full[stage]);
-                    }
-                } else {
-                    mbar_arrive(&sm.full[stage]);
-                }
+                mbar_arrive(&sm.full[stage]);
                 if (++stage == kStages) { stage = 0; sphase ^= 1; }
             }
         }
@@ -704,7 +721,7 @@ int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t
 }
 
 // Kernel instantiation for (reduce, tile height, side projections requested):
-//   max:  {4, 8 rows} x {with, without XZ/YZ}      sum: 4 rows with XZ/YZ, {4, 8} rows XY-only
+//   max: 4 rows {with, without XZ/YZ}, 8 rows with XZ/YZ (projection-only)    sum: 4 rows {with, without}
 template <int INTERP, int FORMULA>
 int launch_variant(bool mx, bool tall, bool side, const CUtensorMap &map, const Params &prm, int grid,
                    cudaStream_t st) {
@@ -712,12 +729,10 @@ int launch_variant(bool mx, bool tall, bool side, const CUtensorMap &map, const 
         if (side)
             return tall ? launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 8, true>(map, prm, grid, st)
                         : launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, true>(map, prm, grid, st);
-        return tall ? launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 8, false>(map, prm, grid, st)
-                    : launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, false>(map, prm, grid, st);
+        return launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, false>(map, prm, grid, st);
     }
     if (side) return launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, true>(map, prm, grid, st);
-    return tall ? launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 8, false>(map, prm, grid, st)
-                : launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
+    return launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
 }
 
 }  // namespace tma_path
@@ -758,7 +773,9 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     const cuuint64_t strides[2] = {(cuuint64_t)row_stride_of(d) * 2, (cuuint64_t)frame_stride_of(d) * 2};
     const bool mx = d.reduce == SSB_REDUCE_MAX;
     const bool side = xz != nullptr || yz != nullptr;
-    const bool tall = vol == nullptr && env_i64("SSB_TALL_TILES", 1) != 0 && (mx || !side);
+    // 8-row tiles pay only where the per-row XZ/YZ work dominates: projection-only max with side
+    // projections (measured: XY-only is faster with 4-row tiles and their deeper 5-stage ring)
+    const bool tall = vol == nullptr && env_i64("SSB_TALL_TILES", 1) != 0 && mx && side;
     const int kTU = tall ? Cfg<8>::kTU : Cfg<4>::kTU;
     const int slack = d.interp == SSB_INTERP_NEAREST ? box_slack<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
                       : d.formula == SSB_FORMULA_CANVAS ? box_slack<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>()

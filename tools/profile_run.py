@@ -19,9 +19,10 @@ ap.add_argument("--hw", type=int, default=2048)
 ap.add_argument("--no-volume", action="store_true")
 ap.add_argument("--formula", default="canvas")
 ap.add_argument("--axes", default="0,1,2")
+ap.add_argument("--alpha", type=float, default=30.0)
 a = ap.parse_args()
 axes = tuple(int(v) for v in a.axes.split(","))
-s = math.cos(math.radians(30.0))
+s = math.cos(math.radians(a.alpha))
 g = torch.Generator(device="cuda").manual_seed(1234)
 raw = torch.randint(0, 4096, (a.n, a.hw, a.hw), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
 res = None
