@@ -1,18 +1,17 @@
 #!/bin/bash
-# A/B timing of prebuilt library variants (variants/libssb_<name>.so), interleaved.
-# usage: tools/ab_variants.sh name1 name2 ...   (run on the GPU box)
-set -e
+# A/B of prebuilt library variants (variants/libssb_<name>.so): GPU parity suite once per
+# variant, then interleaved timing sweeps (tools/time_variants.sh).   usage: tools/ab_variants.sh a b ...
 cd "$(dirname "$0")/.."
 cp paper_2211_00645_b200/lib/libssb.so /tmp/libssb_orig.so
+for v in "$@"; do
+  cp "variants/libssb_$v.so" paper_2211_00645_b200/lib/libssb.so
+  echo "== $v parity: $(timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1)"
+done
 for rep in 1 2; do
   for v in "$@"; do
     cp "variants/libssb_$v.so" paper_2211_00645_b200/lib/libssb.so
     echo "== $v (rep $rep)"
-    python tools/profile_run.py --iters 20
-    python tools/profile_run.py --iters 20 --no-volume
-    python tools/profile_run.py --iters 20 --no-volume --axes 0
-    python tools/profile_run.py --iters 20 --reduce sum
-    python tools/profile_run.py --iters 20 --interp nearest
+    tools/time_variants.sh
   done
 done
 cp /tmp/libssb_orig.so paper_2211_00645_b200/lib/libssb.so
