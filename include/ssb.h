@@ -130,6 +130,18 @@ int ssb_warp_rows(const uint16_t *proj, int64_t rows, int64_t cols, double warp_
 int ssb_combine(const void *src, void *dst, int64_t count, int32_t reduce, int32_t elem_bits,
                 void *stream);
 
+/*
+ * Display encode, gray8 payload.  Replaces the pixel path of encode_frame_packet
+ * (skewstream/server.py:83-91): offset = min, range = max - min over the image;
+ * range == 0 -> all-zero bytes, else dst[k] = rint((src[k] - offset) * (255.0 / range))
+ * in fp64 (numpy's op order).  src: device uint16 (count), dst: device uint8 (count);
+ * stats: device, >= ssb_encode_gray8_stats_bytes(), receives {offset, range} as uint32 in
+ * words 0 and 1 (the header fields g8_offset / g8_range, server.py:84-86).  One launch.
+ */
+size_t ssb_encode_gray8_stats_bytes(void);
+int ssb_encode_gray8(const uint16_t *src, int64_t count, uint8_t *dst, uint32_t *stats, size_t stats_bytes,
+                     void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -236,3 +236,16 @@ def rolling_band(ring: list, shear: float, interp: str, h: int, w: int,
         seg[better] = r[better]
         contrib[olo - lo:ohi - lo + 1][better] = k
     return band, contrib
+
+
+# ---------------------------------------------------------------------------
+# display encode
+
+def encode_gray8(pixels: np.ndarray) -> tuple[np.ndarray, int, int]:
+    """skewstream/server.py:83-91 restated: (payload uint8, g8_offset, g8_range)."""
+    lo, hi = int(pixels.min()), int(pixels.max())
+    rng = hi - lo
+    if rng == 0:
+        return np.zeros(pixels.shape, dtype=np.uint8), lo, 0
+    scaled = (pixels.astype(np.float64) - lo) * (255.0 / rng)
+    return np.rint(scaled).astype(np.uint8), lo, rng

@@ -26,7 +26,8 @@ FLAG_XY_ACCUMULATE = 1
 #: every symbol include/ssb.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ssb_version", "ssb_last_error", "ssb_launch_count", "ssb_profile_enable",
            "ssb_profile_read", "ssb_deskew_workspace_bytes",
-           "ssb_deskew", "ssb_rolling_band", "ssb_warp_rows", "ssb_combine")
+           "ssb_deskew", "ssb_rolling_band", "ssb_warp_rows", "ssb_combine",
+           "ssb_encode_gray8_stats_bytes", "ssb_encode_gray8")
 
 
 class DeskewDesc(ctypes.Structure):
@@ -84,6 +85,9 @@ def load(path: str = LIB_PATH):
         lib.ssb_warp_rows.restype = ctypes.c_int
         lib.ssb_combine.argtypes = [p, p, i64, i32, i32, p]
         lib.ssb_combine.restype = ctypes.c_int
+        lib.ssb_encode_gray8_stats_bytes.restype = ctypes.c_size_t
+        lib.ssb_encode_gray8.argtypes = [p, i64, p, p, ctypes.c_size_t, p]
+        lib.ssb_encode_gray8.restype = ctypes.c_int
         _lib = lib
         return lib
 

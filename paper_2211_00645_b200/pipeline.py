@@ -362,6 +362,24 @@ def deskew_place(canvas: ProjectionCanvas, frame: RawFrame) -> tuple[int, int]:
 
 
 @dataclass(frozen=True)
+class StageTimings:
+    """Per-stack stage durations plus output lag (ss/pipeline.py:118-138)."""
+
+    acquisition_ms: float
+    processing_ms: float
+    plotting_ms: float
+    lag_ms: float
+
+    def __post_init__(self):
+        for name in ("acquisition_ms", "processing_ms", "plotting_ms", "lag_ms"):
+            if getattr(self, name) < 0:
+                raise ParameterError(f"{name} must be >= 0")
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k in ("acquisition_ms", "processing_ms", "plotting_ms", "lag_ms")}
+
+
+@dataclass(frozen=True)
 class DisplayImage:
     """One emitted view (ss/pipeline.py:410-431)."""
 

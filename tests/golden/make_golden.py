@@ -20,6 +20,8 @@ Sources of truth (reference file:line):
 * warp: ``pipeline.warp_projection`` (ss/pipeline.py:434-457)
 * rolling: ``ProjectionCanvas.rolling_replace`` / ``replace_all``
   (ss/pipeline.py:345-398) snapshots of ``max_pixels`` and ``contributor``
+* display packets: ``server.encode_frame_packet`` (ss/server.py:72-117), gray16 and gray8
+  (``--only display`` regenerates just ``display.npz``)
 """
 
 from __future__ import annotations
@@ -214,5 +216,41 @@ def main():
     np.save(os.path.join(fdir, "replayed.npy"), np.stack([src.next_frame().pixels for _ in range(6)]))
 
 
+def display_cases():
+    """display.npz: packets of the reference's encode_frame_packet (own seed)."""
+    from skewstream import server as SV
+    rng = np.random.default_rng(2211)
+    images = [
+        np.array([[0, 100], [200, 1000]]), np.full((3, 4), 1234), np.array([[500, 800], [650, 740]]),
+        np.array([[7]]), rng.integers(0, 65536, (9, 13)), rng.integers(0, 4096, (64, 48)),
+        rng.integers(0, 65536, (60, 257)), 1000 + rng.integers(0, 2, (33, 17)),
+        rng.integers(0, 65536, (1, 1001)), np.arange(65536).reshape(256, 256)[:, ::-1],
+        rng.integers(30000, 30256, (128, 200)),
+    ]
+    out = {}
+    for k, px in enumerate(images):
+        px = np.asarray(px, dtype=np.uint16)
+        timings = PL.StageTimings(4.0 + k, 1.5, 0.25, 6.0 + k / 3) if k % 2 else None
+        tele = {"fps": 12.5 + k, "drops": {"client": k, "server": 1}} if k % 3 == 1 else None
+        img = PL.DisplayImage(pixels=px, channel_id=k % 4, sweep_index=41 + k, slice_index=12 * k,
+                              view_angle_deg=30.0 + 1.337 * k, mode="rolling" if k % 2 else "global",
+                              out_pitch_um=0.115 + 0.001 * k, lateral_pitch_um=0.1, timings=timings)
+        out[f"px_{k}"] = px
+        out[f"meta_{k}"] = np.array([k % 4, 41 + k, 12 * k], dtype=np.int64)
+        out[f"angle_{k}"] = np.float64(30.0 + 1.337 * k)
+        out[f"pitch_{k}"] = np.float64(0.115 + 0.001 * k)
+        out[f"timings_{k}"] = (np.array([4.0 + k, 1.5, 0.25, 6.0 + k / 3]) if timings else np.zeros(0))
+        out[f"tele_{k}"] = (np.array([12.5 + k, k, 1.0]) if tele else np.zeros(0))
+        for fmt in ("gray16", "gray8"):
+            out[f"{fmt}_{k}"] = np.frombuffer(SV.encode_frame_packet(img, pixel_format=fmt, telemetry=tele),
+                                              dtype=np.uint8).copy()
+    out["count"] = np.int64(len(images))
+    np.savez_compressed(os.path.join(HERE, "display.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--only", "display"]:
+        display_cases()
+    else:
+        main()
+        display_cases()
