@@ -22,6 +22,8 @@ Sources of truth (reference file:line):
   (ss/pipeline.py:345-398) snapshots of ``max_pixels`` and ``contributor``
 * display packets: ``server.encode_frame_packet`` (ss/server.py:72-117), gray16 and gray8
   (``--only display`` regenerates just ``display.npz``)
+* live emissions: ``LivePipeline.step`` (ss/pipeline.py:874-980) over scripted frames with
+  view / mode changes (``--only live``)
 """
 
 from __future__ import annotations
@@ -248,9 +250,93 @@ def display_cases():
     np.savez_compressed(os.path.join(HERE, "display.npz"), **out)
 
 
+def live_cases():
+    """live.npz: emissions of the reference's LivePipeline (ss/pipeline.py:706-1064) driven
+    frame by frame with parameter changes at fixed points (own seed)."""
+    from skewstream import geometry as GEO
+    from skewstream.clock import VirtualClock
+    from skewstream.errors import EndOfStream
+
+    rng = np.random.default_rng(645)
+
+    class Script:
+        def __init__(self, g, frames, period_ms):
+            self.geom, self.frames, self.k = g, frames, 0
+            self.period_ns = int(period_ms * 1e6)
+            self.clock = VirtualClock()
+
+        def set_exposure_ms(self, ms):
+            pass
+
+        def next_frame(self):
+            if self.k >= len(self.frames):
+                raise EndOfStream("done")
+            sweep, idx, px = self.frames[self.k]
+            self.k += 1
+            self.clock.sleep_until(self.clock.now_ns() + self.period_ns)
+            return PL.RawFrame(pixels=px, slice_index=idx, sweep_index=sweep, channel_id=0,
+                               timestamp_ns=self.clock.now_ns())
+
+    scenarios = [
+        # (n, h, w, interp, mode, sweeps, changes {frame_count: (kind, value)})
+        (6, 10, 12, "linear", "global", 3, {8: ("angle", 35.0)}),
+        (5, 7, 9, "nearest", "rolling", 3, {4: ("shear", 1.7), 9: ("mode", "global")}),
+        (4, 9, 8, "linear", "global", 4, {3: ("mode", "rolling"), 7: ("angle", 50.0), 11: ("mode", "global")}),
+    ]
+    out = {}
+    for k, (n, h, w, interp, mode, sweeps, changes) in enumerate(scenarios):
+        g = geom(n, h, w)
+        frames = [(sw, i, rng.integers(0, 65536, (h, w)).astype(np.uint16))
+                  for sw in range(sweeps) for i in range(n)]
+        if k == 2:  # drop frames mid-sweep: a partial sweep is abandoned
+            frames = frames[:5] + frames[6:]
+        src = Script(g, frames, 7.0)
+        cfg = PL.PipelineConfig(geom=g, mode=mode, interp=interp)
+        pipe = PL.LivePipeline(src, cfg)
+        vt0 = pipe.vt
+        ems, chg = [], []
+        for step in range(len(frames)):
+            if step in changes:
+                kind, val = changes[step]
+                if kind == "angle":
+                    pipe.post_params(view_angle_deg=val)
+                    vt = GEO.view_transform(g, view_angle_deg=val, out_pitch_um=cfg.out_pitch_um)
+                elif kind == "shear":
+                    pipe.post_params(shear_px=val)
+                    vt = GEO.view_transform(g, shear_px=val, out_pitch_um=cfg.out_pitch_um)
+                else:
+                    pipe.post_params(mode=val)
+                    vt = None
+                chg.append((step, kind, val, vt))
+            for im in pipe.step():
+                ems.append((step, im))
+        out[f"s{k}_meta"] = np.array([n, h, w, sweeps], dtype=np.int64)
+        out[f"s{k}_interp"] = interp
+        out[f"s{k}_mode"] = mode
+        out[f"s{k}_vt0"] = np.array([vt0.shear_px, vt0.warp_scale, vt0.view_angle_deg, vt0.out_pitch_um])
+        out[f"s{k}_frames"] = np.stack([f[2] for f in frames])
+        out[f"s{k}_frame_ids"] = np.array([[f[0], f[1]] for f in frames], dtype=np.int64)
+        out[f"s{k}_changes"] = np.array([[c[0], ["angle", "shear", "mode"].index(c[1]),
+                                          (["global", "rolling"].index(c[2]) if c[1] == "mode" else 0)]
+                                         for c in chg], dtype=np.int64)
+        out[f"s{k}_change_vt"] = np.array([[c[3].shear_px, c[3].warp_scale, c[3].view_angle_deg, c[3].out_pitch_um]
+                                           if c[3] is not None else [0.0] * 4 for c in chg])
+        out[f"s{k}_emit_count"] = np.int64(len(ems))
+        for e, (step, im) in enumerate(ems):
+            out[f"s{k}_e{e}_px"] = im.pixels
+            out[f"s{k}_e{e}_ids"] = np.array([step, im.sweep_index, im.slice_index,
+                                              ["global", "rolling"].index(im.mode)], dtype=np.int64)
+            out[f"s{k}_e{e}_f"] = np.array([im.view_angle_deg, im.out_pitch_um, im.lateral_pitch_um,
+                                            im.timings.acquisition_ms])
+        print(f"live scenario {k}: {len(frames)} frames, {len(ems)} emissions", file=sys.stderr)
+    out["count"] = np.int64(len(scenarios))
+    np.savez_compressed(os.path.join(HERE, "live.npz"), **out)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["--only", "display"]:
-        display_cases()
+    if sys.argv[1:2] == ["--only"]:
+        {"display": display_cases, "live": live_cases}[sys.argv[2]]()
     else:
         main()
         display_cases()
+        live_cases()
