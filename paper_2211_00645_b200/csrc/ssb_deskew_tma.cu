@@ -181,46 +181,61 @@ __device__ __forceinline__ uint4 voxels8(const uint4 a, const uint4 b, const Row
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-// Tap conversion for the chained canvas path.  SSB_NATIVE_CVT: native I2F.F64 conversions (one
-// conversion-pipe op per tap value, measured 16/clk/SM on B200 -- the path needs ~6.5/clk at
-// roofline) and plain DMUL products, fl(w*a).  With SSB_MAGIC_CVT: the 2^52 trick (integer
-// extract + constant high word, DFMA with -w*2^52).  Both round exactly like numpy; measured
-// on B200 the magic form is equal with a volume and 2-3 % faster projection-only, so it is
-// the default.
-#if !defined(SSB_MAGIC_CVT) && !defined(SSB_NATIVE_CVT)
-#define SSB_MAGIC_CVT
+// Tap conversion for the chained canvas path (SSB_CVT_MODE):
+//   0  2^52 trick for every tap value: integer extract + constant high word, DFMA with -w*2^52;
+//   1  native I2F.F64 for every value (one conversion-pipe op, ~16/clk/SM on B200) + DMUL;
+//   2  mixed: low halves native (I2F.F64.U16 reads the half in place, no extract), high halves
+//      by the trick -- 1.5 issue slots per value and half the conversion-pipe load of mode 1.
+// All three give fl(w*a) exactly.  Measured on B200 (profiles/README.md): mode 2 is 2.6-3.4 %
+// faster than mode 0 projection-only and equal with a volume; mode 1 is slowest (conversion pipe).
+#ifndef SSB_CVT_MODE
+#define SSB_CVT_MODE 2
 #endif
-#ifdef SSB_NATIVE_CVT
+template <int C>
+__device__ __forceinline__ constexpr bool native_tap() {
+    return SSB_CVT_MODE == 1 || (SSB_CVT_MODE == 2 && (C & 1) == 0);
+}
+
+// I2F.F64.U16 of the low half of a 32-bit register (no separate extract)
+__device__ __forceinline__ double u16lo_to_f64(uint32_t w) {
+    double r;
+    asm("cvt.rn.f64.u16 %0, %1;" : "=d"(r) : "h"((unsigned short)w));
+    return r;
+}
+
 __device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
     const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        o[2 * q] = __uint2double_rn(w4[q] & 0xFFFFu);
-        o[2 * q + 1] = __uint2double_rn(w4[q] >> 16);
+        o[2 * q] = (SSB_CVT_MODE != 0) ? u16lo_to_f64(w4[q]) : biased(w4[q] & 0xFFFFu);
+        o[2 * q + 1] = (SSB_CVT_MODE == 1) ? __uint2double_rn(w4[q] >> 16) : biased(w4[q] >> 16);
     }
 }
-__device__ __forceinline__ double tap_prod(double c, double a, double /*n*/) { return __dmul_rn(c, a); }
-#else
-// 8 packed uint16 -> 8 doubles 2^52 + v (exact; one integer op + the constant high word each)
-__device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
-    const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        o[2 * q] = biased(w4[q] & 0xFFFFu);
-        o[2 * q + 1] = biased(w4[q] >> 16);
-    }
+
+template <int C>
+__device__ __forceinline__ double tap_prod(double c, double a, double n) {
+    if (native_tap<C>()) return __dmul_rn(c, a);
+    return __fma_rn(c, a, n);
 }
-__device__ __forceinline__ double tap_prod(double c, double a, double n) { return __fma_rn(c, a, n); }
-#endif
 
 // canvas lerp of 8 voxels from converted taps: rint(fl(fl(w0*a) + fl(f*b))) as 8 u32 values
+template <int C>
+__device__ __forceinline__ uint32_t lerp_one(const double a, const double b, const double c0, const double c1,
+                                             const double n0, const double n1) {
+    return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(tap_prod<C>(c0, a, n0), tap_prod<C>(c1, b, n1)), kRintMagic));
+}
+
 __device__ __forceinline__ void lerp_biased8_raw(const double (&a)[8], const double (&b)[8], const double c0,
                                                  const double c1, const double n0, const double n1,
                                                  uint32_t (&r)[8]) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-        r[c] = (uint32_t)__double2loint(
-            __dadd_rn(__dadd_rn(tap_prod(c0, a[c], n0), tap_prod(c1, b[c], n1)), kRintMagic));
+    r[0] = lerp_one<0>(a[0], b[0], c0, c1, n0, n1);
+    r[1] = lerp_one<1>(a[1], b[1], c0, c1, n0, n1);
+    r[2] = lerp_one<2>(a[2], b[2], c0, c1, n0, n1);
+    r[3] = lerp_one<3>(a[3], b[3], c0, c1, n0, n1);
+    r[4] = lerp_one<4>(a[4], b[4], c0, c1, n0, n1);
+    r[5] = lerp_one<5>(a[5], b[5], c0, c1, n0, n1);
+    r[6] = lerp_one<6>(a[6], b[6], c0, c1, n0, n1);
+    r[7] = lerp_one<7>(a[7], b[7], c0, c1, n0, n1);
 }
 
 __device__ __forceinline__ uint4 pack8(const uint32_t (&r)[8]) {
