@@ -263,6 +263,12 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ uint4 max3_u16x8(const uint4 a, const uint4 b, const uint4 c) {
+    // __vmaxu2(__vmaxu2(.)) pairs fuse into one VIMNMX3.U16x2 each
+    return make_uint4(__vmaxu2(__vmaxu2(a.x, b.x), c.x), __vmaxu2(__vmaxu2(a.y, b.y), c.y),
+                      __vmaxu2(__vmaxu2(a.z, b.z), c.z), __vmaxu2(__vmaxu2(a.w, b.w), c.w));
+}
+
 __device__ __forceinline__ uint32_t hmax8(const uint4 v) {
     const uint32_t m = __vmaxu2(__vmaxu2(__vmaxu2(v.x, v.y), v.z), v.w);  // ptxas fuses into VIMNMX3
     return max(m & 0xFFFFu, m >> 16);
@@ -328,6 +334,9 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                                           uint4 (&acc_max)[ROWS], uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
                                           uint4 &xz_max, uint32_t (&xz_sum)[8], uint32_t (&yzv)[ROWS]) {
     constexpr bool kStream = ROWS > 4 || (!kMax && !SIDE);
+    constexpr bool kFoldXz = kMax && SIDE && !kStream;  // XZ over the batch with 3-input maxes
+    constexpr bool kPairXz = kMax && SIDE && kStream;   // XZ over row pairs with 3-input maxes
+    uint4 xz_prev = make_uint4(0, 0, 0, 0);
     const bool store = vrow != nullptr;
     constexpr bool chain = CHAIN && INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS;
     auto consume = [&](const int k, const uint4 v) {
@@ -335,7 +344,12 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         if (kMax) {
             acc_max[k] = max_u16x8(acc_max[k], v);
             if (SIDE) {  // XZ / YZ requested (compile-time: XY-only views skip this work)
-                xz_max = max_u16x8(xz_max, v);
+                if (kPairXz) {
+                    if (k & 1) xz_max = max3_u16x8(xz_max, xz_prev, v);
+                    else xz_prev = v;
+                } else if (!kFoldXz) {
+                    xz_max = max_u16x8(xz_max, v);
+                }
                 yzv[k] = redux_max(hmax8(v));
             }
         } else {
@@ -394,6 +408,10 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         else vs[k] = v;
     }
     if (!kStream) {
+        if (kFoldXz) {
+#pragma unroll
+            for (int k = 0; k + 1 < ROWS; k += 2) xz_max = max3_u16x8(xz_max, vs[k], vs[k + 1]);
+        }
 #pragma unroll
         for (int k = 0; k < ROWS; ++k) consume(k, vs[k < (kStream ? 1 : ROWS) ? k : 0]);
     }
