@@ -96,6 +96,8 @@ struct Params {
     double shear;
     int64_t n1, chunk2;  // phase split: slices [0, n1) in chunks of `chunk`, [n1, n) of `chunk2`
     int32_t UT, XT, S, S2, n_items, xy_accumulate;
+    int32_t clip;        // projection-only: each u-tile visits only the slices that can touch it
+    int32_t big_pct;     // (clip) phase-1 share of a tile's slice range, percent
 };
 
 template <int ROWS>
@@ -114,29 +116,58 @@ struct Smem {
     int32_t queue[kQueue];
 };
 
+// Slices whose span can touch canvas rows [tu0, tu0 + TU): slice g covers about
+// [g*s - 1, g*s + H] under both interpolations, so the bounds below (2 rows of margin) are
+// conservative; the producer still tests every slice exactly.
+template <int TU>
+__device__ __forceinline__ void tile_slices(const Params &p, int ut, int64_t &lo, int64_t &hi) {
+    lo = 0;
+    hi = p.n;
+    if (!(p.shear > 0.0)) return;
+    const double tu0 = (double)(p.u_begin + (int64_t)ut * TU);
+    const double first = (double)p.first, n = (double)p.n;
+    // clamp in fp64 before converting (tiny shears give huge quotients)
+    const double glo = fmin(fmax(floor((tu0 - (double)p.h - 2.0) / p.shear) - first, 0.0), n);
+    const double ghi = fmin(fmax(floor((tu0 + (double)(TU + 1)) / p.shear) + 1.0 - first, glo), n);
+    lo = (int64_t)glo;
+    hi = (int64_t)ghi;
+}
+
 // Work item -> (u-tile, x-tile, slice range).  Two phases: every tile's first n1 slices in
 // big chunks, then the remaining slices in small chunks, so the dynamic scheduler ends on
 // short items (tail balance).  Within a phase u-tiles go centre-out (heaviest first).
+// Projection-only launches (p.clip) split each tile's own slice range instead of [0, n): a
+// long scan's tile is touched by ~(H + TU)/s of its slices, the rest would be empty stages.
+template <int TU>
 __device__ __forceinline__ void decode(int item, const Params &p, int &ut, int &xt, int64_t &s_begin,
                                        int64_t &s_end) {
     const int items1 = p.UT * p.XT * p.S;
-    int S = p.S, sc;
-    int64_t chunk = p.chunk, base = 0, stop = p.n1;
-    if (item >= items1) {
-        item -= items1;
-        S = p.S2;
-        chunk = p.chunk2;
-        base = p.n1;
-        stop = p.n;
-    }
-    sc = item % S;
+    const bool tail = item >= items1;
+    if (tail) item -= items1;
+    const int S = tail ? p.S2 : p.S;
+    const int sc = item % S;
     const int rest = item / S;
     xt = rest % p.XT;
     const int k = rest / p.XT;
     const int mid = (p.UT - 1) / 2;
     const int d = (k + 1) >> 1;
     ut = (k & 1) ? mid + d : mid - d;
-    s_begin = base + (int64_t)sc * chunk;
+    int64_t chunk, base, stop;
+    if (p.clip) {
+        int64_t lo, hi;
+        tile_slices<TU>(p, ut, lo, hi);
+        const int64_t L = hi - lo;
+        const int64_t n1 = p.S2 > 0 ? (L * p.big_pct) / 100 : L;
+        base = tail ? lo + n1 : lo;
+        stop = tail ? hi : lo + n1;
+        chunk = (stop - base + S - 1) / S;
+        if (chunk < 1) chunk = 1;
+    } else {
+        chunk = tail ? p.chunk2 : p.chunk;
+        base = tail ? p.n1 : 0;
+        stop = tail ? p.n : p.n1;
+    }
+    s_begin = min(stop, base + (int64_t)sc * chunk);
     s_end = min(stop, s_begin + chunk);
 }
 
@@ -463,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (done) break;
             int ut, xt;
             int64_t s_begin, s_end;
-            decode(item, p, ut, xt, s_begin, s_end);
+            decode<kTU>(item, p, ut, xt, s_begin, s_end);
             const int64_t tu0 = p.u_begin + (int64_t)ut * kTU;
             for (int64_t s = s_begin; s < s_end; ++s) {
                 int64_t lo, hi;
@@ -545,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         int ut, xt;
         int64_t s_begin, s_end;
-        decode(item, p, ut, xt, s_begin, s_end);
+        decode<kTU>(item, p, ut, xt, s_begin, s_end);
         const int64_t x = (int64_t)xt * kTX + lane * 8;
         const bool col_ok = x < p.w;
         const int64_t r0 = (int64_t)ut * kTU + warp * ROWS;  // window row of k = 0
@@ -835,11 +866,16 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
         S = n_sl > 0 ? (n_sl + chunk - 1) / chunk : 0;
     };
     const int64_t big_pct = std::min<int64_t>(100, std::max<int64_t>(0, env_i64("SSB_BIG_PERCENT", 85)));
-    int64_t n1 = d.n * big_pct / 100;
-    if (n1 < 1) n1 = d.n;
+    // projection-only: tiles visit only the slices that can touch them (no volume zero fill
+    // to write), so the chunking is planned on the longest per-tile slice range
+    const bool clip = vol == nullptr && d.shear_px > 0.0 && env_i64("SSB_CLIP_SLICES", 1) != 0;
+    const double span_slices = std::ceil((kTU + d.height + 4) / d.shear_px) + 2.0;
+    const int64_t n_plan = clip && span_slices < (double)d.n ? (int64_t)span_slices : d.n;
+    int64_t n1 = n_plan * big_pct / 100;
+    if (n1 < 1) n1 = n_plan;
     int64_t S, chunk, S2, chunk2;
     split(n1, env_i64("SSB_ITEMS_PER_CTA", 2), S, chunk);
-    split(d.n - n1, env_i64("SSB_TAIL_ITEMS_PER_CTA", 6), S2, chunk2);
+    split(n_plan - n1, env_i64("SSB_TAIL_ITEMS_PER_CTA", 6), S2, chunk2);
     const int64_t items = tiles * (S + S2);
     if (items > INT32_MAX / 2) return fail(SSB_ERR_CAPACITY, "too many tiles");
 
@@ -888,6 +924,8 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     prm.S = (int32_t)S;
     prm.n_items = (int32_t)items;
     prm.xy_accumulate = acc;
+    prm.clip = clip ? 1 : 0;
+    prm.big_pct = (int32_t)big_pct;
     const int grid = (int)std::min<int64_t>(items, sms);
 
     int rc;
