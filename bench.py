@@ -307,9 +307,22 @@ def run_ours(args, cfg, rank, world, local_rank):
             t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t[0])
+        # the bound of this number: a plain pinned 256 MiB H2D copy on this box, measured now
+        probe_h = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+        probe_d = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        probe_d.copy_(probe_h, non_blocking=True)
+        a0.record(stream)
+        for _ in range(4):
+            probe_d.copy_(probe_h, non_blocking=True)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ceiling = 4 * (256 << 20) / (a0.elapsed_time(a1) * 1e-3) / 1e9
+        del probe_h, probe_d
+        h2d = 2 * n * h * w
         e2e = {"value": world * vox / (e_ms * 1e-3) / 1e9, "unit": "GVoxels/s",
-               "h2d_bytes_per_step": 2 * n * h * w, "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in projs.values()),
-               "ms_per_step": e_ms, "path": "stream.StackStreamer.run (pinned host -> 2 copy streams -> ssb_deskew per chunk) + projections D2H; volume stays in HBM"}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in projs.values()),
+               "ms_per_step": e_ms, "h2d_gbs": h2d / (e_ms * 1e-3) / 1e9, "h2d_copy_ceiling_gbs": ceiling,
+               "path": "stream.StackStreamer.run (pinned host -> 2 copy streams -> ssb_deskew per chunk) + projections D2H; volume stays in HBM"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

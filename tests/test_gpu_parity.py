@@ -519,3 +519,32 @@ def test_deskew_volume_device_api():
     want_vol, want = C.deskew(st, 0.73, "nearest", reduce="sum")
     np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
     np.testing.assert_array_equal(res.xz.cpu().numpy(), want[1])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_projection_only_long_scans_and_slabs(seed):
+    """Projection-only launches walk each u-tile's own slice range (conservative span bounds):
+    long scans with small shears, tiny / zero / large shears, and slab windows with global
+    slice indices, against the C oracle's full volume."""
+    rng = np.random.default_rng(4200 + seed)
+    n, h = int(rng.integers(150, 420)), int(rng.integers(20, 90))
+    w = 8 * int(rng.integers(1, 40))
+    s = [0.05, 1e-7, 0.0, 3.3, 0.7071067811865476, 0.31][seed]
+    st = rng.integers(0, 65536, (n, h, w)).astype(np.uint16)
+    interp = "linear" if seed % 2 == 0 else "nearest"
+    for reduce in ("max", "sum"):
+        full_vol, _ = C.deskew(st, s, interp, reduce=reduce)
+        U = full_vol.shape[1]
+        a, b = int(rng.integers(0, n // 3)), int(rng.integers(2 * n // 3, n + 1))
+        lo = O.span(a, s, h, interp)[0]
+        hi = O.span(b - 1, s, h, interp)[1]
+        ref = full_vol[a:b, lo:hi + 1]
+        for axes in ((0,), (0, 1, 2)):
+            _, pr = run(st[a:b], s, interp, reduce=reduce, first_slice=a, canvas_rows=U, u_begin=lo,
+                        u_count=hi - lo + 1, write_volume=False, projection_axes=axes)
+            for ax in axes:
+                np.testing.assert_array_equal(pr[ax], O.project(ref, ax, reduce), err_msg=f"{reduce} {axes} ax{ax}")
+        # whole scan
+        _, pr = run(st, s, interp, reduce=reduce, write_volume=False, projection_axes=(0, 1, 2))
+        for ax in (0, 1, 2):
+            np.testing.assert_array_equal(pr[ax], O.project(full_vol, ax, reduce))
