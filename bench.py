@@ -52,6 +52,9 @@ def canvas_rows(n, h, s):
     return h + math.ceil((n - 1) * s - 1e-9)
 
 
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e datasheet bandwidth (SURVEY.md §8(d) asks for both)
+
+
 def peaks():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -341,6 +344,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                        "parallelism": f"dp{world} (stacks)", "l2": "inputs 4.3 GB and outputs 5.2 GB >> 126 MB L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "spec_peak": SPEC_HBM_GBS, "frac_of_spec": achieved / SPEC_HBM_GBS,
                          "bytes_per_launch": bytes_launch, "kernel_ms": kern_avg,
                          "kernel": "deskew_tma_kernel (TMA-pipelined persistent)"},
             "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
