@@ -108,12 +108,15 @@ int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_t *vol, voi
  * ring slot k holds global slice k; canvas (U, W) uint16, contributor (U, W) int16.
  * replaced >= 0: only ring slot `replaced` changed since canvas/contributor were
  * last consistent, so voxels it did not contribute to are updated in O(1)
- * (exactly equal to the full re-max); replaced < 0: full recompute of the band.
+ * (exactly equal to the full re-max) and the ones it did are re-maxed over the ring
+ * (device workspace >= ssb_rolling_workspace_bytes(hi - lo + 1, W) holds their list);
+ * replaced < 0: full recompute of the band (no workspace needed).
  */
+size_t ssb_rolling_workspace_bytes(int64_t band_rows, int64_t width);
 int ssb_rolling_band(const uint16_t *ring, const uint8_t *present, int64_t n_ring, int64_t height,
                      int64_t width, double shear_px, int32_t interp, int64_t lo, int64_t hi,
                      uint16_t *canvas, int16_t *contributor, int64_t canvas_rows, int64_t replaced,
-                     void *stream);
+                     void *workspace, size_t workspace_bytes, void *stream);
 
 /*
  * Display warp.  Replaces warp_projection (ss/pipeline.py:434-457): out row m

@@ -78,45 +78,32 @@ __device__ __forceinline__ uint32_t ring_offer(const uint16_t *__restrict__ ring
     return rp.kind == 2 ? lerp_voxel<SSB_FORMULA_CANVAS>(a, frame[(size_t)rp.j1 * w + x], rp) : a;
 }
 
-// ss/pipeline.py:361-377.  One thread per (row, column) of the band.  Strict '>' in
-// ring order keeps the first maximum; contributor -1 where every offer is 0.
-//
-// Incremental form (replaced = k >= 0, canvas exact before slot k changed): a voxel
-// whose contributor is not k keeps its maximum unless the new offer v of slot k beats
-// it -- v > best, or v == best > 0 with k earlier in ring order -- which is exactly the
-// full re-max (every other slot's offer is unchanged and <= best, with ties only at
-// later ring indices).  Voxels that k contributed to are re-maxed over the whole ring.
+// Slots whose span can contain canvas row u: i*s within [u-H-1, u+1] (exact check in ring_offer).
+__device__ __forceinline__ void ring_range(int64_t u, int64_t n_ring, int64_t h, double s, int64_t &k_lo,
+                                           int64_t &k_hi) {
+    k_lo = 0;
+    k_hi = n_ring - 1;
+    if (s > 0.0) {
+        const double kl = floor(((double)(u - h) - 2.0) / s);
+        const double kh = ceil(((double)u + 2.0) / s);
+        k_lo = kl <= 0.0 ? 0 : (kl >= (double)n_ring ? n_ring : (int64_t)kl);
+        k_hi = kh >= (double)(n_ring - 1) ? n_ring - 1 : (kh < 0.0 ? -1 : (int64_t)kh);
+    }
+}
+
+// ss/pipeline.py:361-377, full recompute of a band.  One thread per (row, column).  Strict
+// '>' in ring order keeps the first maximum; contributor -1 where every offer is 0.
 template <int INTERP>
-__global__ void rolling_band_kernel(const uint16_t *__restrict__ ring, const uint8_t *__restrict__ present,
-                                    int64_t n_ring, int64_t h, int64_t w, double s, int64_t lo,
-                                    int64_t hi, uint16_t *__restrict__ canvas,
-                                    int16_t *__restrict__ contrib, int64_t replaced) {
+__global__ void rolling_full_kernel(const uint16_t *__restrict__ ring, const uint8_t *__restrict__ present,
+                                    int64_t n_ring, int64_t h, int64_t w, double s, int64_t lo, int64_t hi,
+                                    uint16_t *__restrict__ canvas, int16_t *__restrict__ contrib) {
     const int64_t total = (hi - lo + 1) * w;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t u = lo + e / w;
         const int64_t x = e % w;
-        const size_t idx = (size_t)u * w + x;
-        if (replaced >= 0) {
-            const int32_t who = contrib[idx];
-            if (who != replaced) {
-                const uint32_t best = canvas[idx];
-                const uint32_t v = ring_offer<INTERP>(ring, present, replaced, u, x, h, w, s);
-                if (v > best || (v == best && v > 0 && replaced < who)) {
-                    canvas[idx] = (uint16_t)v;
-                    contrib[idx] = (int16_t)replaced;
-                }
-                continue;
-            }
-        }
-        // slices whose span can contain u: i*s within [u-H-1, u+1] (exact check in ring_offer)
-        int64_t k_lo = 0, k_hi = n_ring - 1;
-        if (s > 0.0) {
-            const double kl = floor(((double)(u - h) - 2.0) / s);
-            const double kh = ceil(((double)u + 2.0) / s);
-            k_lo = kl <= 0.0 ? 0 : (kl >= (double)n_ring ? n_ring : (int64_t)kl);
-            k_hi = kh >= (double)(n_ring - 1) ? n_ring - 1 : (kh < 0.0 ? -1 : (int64_t)kh);
-        }
+        int64_t k_lo, k_hi;
+        ring_range(u, n_ring, h, s, k_lo, k_hi);
         uint32_t best = 0;
         int32_t who = -1;
         for (int64_t k = k_lo; k <= k_hi; ++k) {
@@ -126,8 +113,74 @@ __global__ void rolling_band_kernel(const uint16_t *__restrict__ ring, const uin
                 who = (int32_t)k;
             }
         }
-        canvas[idx] = (uint16_t)best;
-        contrib[idx] = (int16_t)who;
+        canvas[(size_t)u * w + x] = (uint16_t)best;
+        contrib[(size_t)u * w + x] = (int16_t)who;
+    }
+}
+
+// Incremental pass (replaced = k, canvas exact before slot k changed): a voxel whose
+// contributor is not k keeps its maximum unless the new offer v of slot k beats it -- v > best,
+// or v == best > 0 with k earlier in ring order -- which is exactly the full re-max (every
+// other slot's offer is unchanged and <= best, with ties only at later ring indices).  Voxels
+// that k contributed to need the whole ring: they are appended to a list (a few per thousand:
+// one slot of the ~H/s overlapping ones is each voxel's maximum) for rolling_remax_kernel, so
+// no warp serialises a ring-long loop behind one lane.
+template <int INTERP>
+__global__ void rolling_incr_kernel(const uint16_t *__restrict__ ring, const uint8_t *__restrict__ present,
+                                    int64_t n_ring, int64_t h, int64_t w, double s, int64_t lo, int64_t hi,
+                                    uint16_t *__restrict__ canvas, int16_t *__restrict__ contrib, int32_t replaced,
+                                    uint32_t *__restrict__ list, uint32_t *__restrict__ count) {
+    const int64_t total = (hi - lo + 1) * w;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = lo + e / w;
+        const int64_t x = e % w;
+        const size_t idx = (size_t)u * w + x;
+        const int32_t who = contrib[idx];
+        if (who == replaced) {
+            list[atomicAdd(count, 1u)] = (uint32_t)e;
+            continue;
+        }
+        const uint32_t best = canvas[idx];
+        const uint32_t v = ring_offer<INTERP>(ring, present, replaced, u, x, h, w, s);
+        if (v > best || (v == best && v > 0 && replaced < who)) {
+            canvas[idx] = (uint16_t)v;
+            contrib[idx] = (int16_t)replaced;
+        }
+    }
+}
+
+// Full re-max of the listed voxels: one warp per voxel, lanes over ring slots (32 at a time),
+// first maximum by a max then a min-index reduction.
+template <int INTERP>
+__global__ void rolling_remax_kernel(const uint16_t *__restrict__ ring, const uint8_t *__restrict__ present,
+                                     int64_t n_ring, int64_t h, int64_t w, double s, int64_t lo,
+                                     uint16_t *__restrict__ canvas, int16_t *__restrict__ contrib,
+                                     const uint32_t *__restrict__ list, const uint32_t *__restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = *count;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
+        const int64_t e = list[i];
+        const int64_t u = lo + e / w;
+        const int64_t x = e % w;
+        int64_t k_lo, k_hi;
+        ring_range(u, n_ring, h, s, k_lo, k_hi);
+        uint32_t best = 0;
+        int32_t who = -1;
+        for (int64_t k0 = k_lo; k0 <= k_hi; k0 += 32) {
+            const int64_t k = k0 + lane;
+            const uint32_t v = k <= k_hi ? ring_offer<INTERP>(ring, present, k, u, x, h, w, s) : 0u;
+            const uint32_t m = __reduce_max_sync(0xffffffffu, v);
+            if (m > best) {  // strict: an equal maximum in a later chunk keeps the earlier slot
+                best = m;
+                who = (int32_t)__reduce_min_sync(0xffffffffu, v == m ? (uint32_t)k : 0xFFFFFFFFu);
+            }
+        }
+        if (lane == 0) {
+            canvas[(size_t)u * w + x] = (uint16_t)best;
+            contrib[(size_t)u * w + x] = (int16_t)who;
+        }
     }
 }
 
@@ -199,10 +252,15 @@ extern "C" int ssb_profile_read(double *total_ms, int64_t *launches) {
     return SSB_OK;
 }
 
+extern "C" size_t ssb_rolling_workspace_bytes(int64_t band_rows, int64_t width) {
+    return 256 + (size_t)std::max<int64_t>(0, band_rows) * (size_t)std::max<int64_t>(0, width) * 4;
+}
+
 extern "C" int ssb_rolling_band(const uint16_t *ring, const uint8_t *present, int64_t n_ring,
                                 int64_t height, int64_t width, double shear_px, int32_t interp,
                                 int64_t lo, int64_t hi, uint16_t *canvas, int16_t *contributor,
-                                int64_t canvas_rows, int64_t replaced, void *stream) {
+                                int64_t canvas_rows, int64_t replaced, void *workspace, size_t workspace_bytes,
+                                void *stream) {
     if (n_ring < 1 || height < 1 || width < 1) return fail(SSB_ERR_PARAM, "bad ring shape");
     if (!(shear_px >= 0.0)) return fail(SSB_ERR_PARAM, "shear_px must be >= 0");
     if (interp != SSB_INTERP_NEAREST && interp != SSB_INTERP_LINEAR)
@@ -213,14 +271,39 @@ extern "C" int ssb_rolling_band(const uint16_t *ring, const uint8_t *present, in
     if (replaced >= n_ring || n_ring > 32767) return fail(SSB_ERR_PARAM, "ring index out of range");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t total = (hi - lo + 1) * width;
-    if (interp == SSB_INTERP_NEAREST)
-        rolling_band_kernel<SSB_INTERP_NEAREST><<<grid_for(total, 256), 256, 0, st>>>(
-            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor, replaced);
-    else
-        rolling_band_kernel<SSB_INTERP_LINEAR><<<grid_for(total, 256), 256, 0, st>>>(
-            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor, replaced);
-    count_launches(1);
-    return check_launch("rolling_band_kernel");
+    if (replaced < 0) {
+        if (interp == SSB_INTERP_NEAREST)
+            rolling_full_kernel<SSB_INTERP_NEAREST><<<grid_for(total, 256), 256, 0, st>>>(
+                ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor);
+        else
+            rolling_full_kernel<SSB_INTERP_LINEAR><<<grid_for(total, 256), 256, 0, st>>>(
+                ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor);
+        count_launches(1);
+        return check_launch("rolling_full_kernel");
+    }
+    if (total > (int64_t)UINT32_MAX) return fail(SSB_ERR_CAPACITY, "band too large");
+    if (workspace == nullptr || workspace_bytes < ssb_rolling_workspace_bytes(hi - lo + 1, width))
+        return fail(SSB_ERR_CAPACITY, "rolling workspace too small: need %zu bytes",
+                    ssb_rolling_workspace_bytes(hi - lo + 1, width));
+    uint32_t *count = static_cast<uint32_t *>(workspace);
+    uint32_t *list = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + 256);
+    cudaMemsetAsync(count, 0, 4, st);
+    const int remax_blocks = num_sms() * 8;
+    if (interp == SSB_INTERP_NEAREST) {
+        rolling_incr_kernel<SSB_INTERP_NEAREST><<<grid_for(total, 256), 256, 0, st>>>(
+            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor, (int32_t)replaced, list,
+            count);
+        rolling_remax_kernel<SSB_INTERP_NEAREST><<<remax_blocks, 256, 0, st>>>(
+            ring, present, n_ring, height, width, shear_px, lo, canvas, contributor, list, count);
+    } else {
+        rolling_incr_kernel<SSB_INTERP_LINEAR><<<grid_for(total, 256), 256, 0, st>>>(
+            ring, present, n_ring, height, width, shear_px, lo, hi, canvas, contributor, (int32_t)replaced, list,
+            count);
+        rolling_remax_kernel<SSB_INTERP_LINEAR><<<remax_blocks, 256, 0, st>>>(
+            ring, present, n_ring, height, width, shear_px, lo, canvas, contributor, list, count);
+    }
+    count_launches(2);
+    return check_launch("rolling_incr_kernel / rolling_remax_kernel");
 }
 
 extern "C" int ssb_warp_rows(const uint16_t *proj, int64_t rows, int64_t cols, double warp_scale,

@@ -138,6 +138,7 @@ class ProjectionCanvas:
         self._ring: list = [None] * geom.slice_count
         self._ring_dev = None      # (N, H, W) uint16, allocated on first rolling use
         self._present_dev = None   # (N,) uint8
+        self._roll_ws = None       # device list of voxels to re-max (incremental rolling updates)
         self._host_cache = None
         # True while canvas + contributor equal the full re-max over the ring, so a
         # rolling_replace can take the O(band) incremental path (see ssb_rolling_band)
@@ -307,8 +308,12 @@ class ProjectionCanvas:
             if self._ring_dev is None or tuple(self._ring_dev.shape) != (n, h, w):
                 self._ring_dev = torch.zeros((n, h, w), dtype=torch.uint16, device=self._device)
                 self._present_dev = torch.zeros((n,), dtype=torch.uint8, device=self._device)
-            self._ring_dev[frame.slice_index].copy_(torch.from_numpy(np.ascontiguousarray(frame.pixels)))
+            host = torch.from_numpy(np.ascontiguousarray(frame.pixels))
+            pinned = host.is_pinned()
+            self._ring_dev[frame.slice_index].copy_(host, non_blocking=pinned)
             self._present_dev[frame.slice_index] = 1
+        if pinned:
+            self._pending_upload = host  # the async copy may still read it (see _upload)
 
     def rolling_replace(self, frame: RawFrame) -> tuple[int, int]:
         """Swap in the newest version of a slice and refresh its band (ss/pipeline.py:345-359)."""
@@ -328,11 +333,18 @@ class ProjectionCanvas:
         full ring re-max (``_exact``); otherwise the whole band is re-maxed.
         """
         lib = _lib.load()
+        ws, ws_bytes = None, 0
+        if replaced >= 0:
+            ws_bytes = int(lib.ssb_rolling_workspace_bytes(hi - lo + 1, self.width))
+            if self._roll_ws is None or self._roll_ws.numel() < ws_bytes:
+                with torch.cuda.stream(self.stream):
+                    self._roll_ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self._device)
+            ws = self._roll_ws
         _lib.check(lib.ssb_rolling_band(
             _vp(self._ring_dev), _vp(self._present_dev), self.geom.slice_count,
             self.geom.frame_height_px, self.width, self.shear_px, _lib.INTERP[self.interp], lo, hi,
             _vp(self.max_pixels_device), _vp(self.contributor_device), self.height, replaced,
-            ctypes.c_void_p(self.stream.cuda_stream)))
+            _vp(ws), ws_bytes, ctypes.c_void_p(self.stream.cuda_stream)))
         self._host_cache = None
         self._canvas_zero = False
 
