@@ -225,20 +225,49 @@ def run_ours(args, cfg, rank, world, local_rank):
              1: torch.empty((n, w), dtype=torch.uint16, device=dev),
              2: torch.empty((n, u), dtype=torch.uint16, device=dev)}
     gather = [torch.empty((u, 2 * w), dtype=torch.uint8, device=dev) for _ in range(world)] if world > 1 and rank == 0 else None
+    # N > 1: each stack's XY goes to the display rank (NCCL gather over NVLink).  The gather of
+    # step k runs on a side stream while step k+1 deskews into the other XY buffer.
+    overlap = world > 1 and not args.no_gather_overlap
+    xy_bufs = [projs[0], torch.empty_like(projs[0])] if overlap else [projs[0]]
+    comm = torch.cuda.Stream(dev) if overlap else None
+    pending = [None, None]
+    counter = [0]
 
     def step():
-        deskew_device(raw, s, interp, reduce=reduce, volume=vol, projections=projs, stream=stream)
-        if world > 1:
-            dist.gather(projs[0].view(torch.uint8), gather, dst=0)
+        b = counter[0] % len(xy_bufs)
+        counter[0] += 1
+        if pending[b] is not None:
+            with torch.cuda.stream(stream):
+                pending[b].wait()  # the gather that read this buffer has finished
+            pending[b] = None
+        deskew_device(raw, s, interp, reduce=reduce, volume=vol, projections={0: xy_bufs[b], 1: projs[1], 2: projs[2]},
+                      stream=stream)
+        if world > 1 and not overlap:
+            dist.gather(xy_bufs[b].view(torch.uint8), gather, dst=0)
+        elif overlap:
+            ready = torch.cuda.Event()
+            ready.record(stream)
+            with torch.cuda.stream(comm):
+                comm.wait_event(ready)
+                pending[b] = dist.gather(xy_bufs[b].view(torch.uint8), gather, dst=0, async_op=True)
+
+    def drain():
+        for b in range(len(pending)):
+            if pending[b] is not None:
+                with torch.cuda.stream(stream):
+                    pending[b].wait()
+                pending[b] = None
 
     for _ in range(args.warmup):
         step()
+    drain()
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
     t_heat = time.perf_counter()
     while time.perf_counter() - t_heat < args.heat_seconds:  # untimed: lets clocks settle / be sampled
         step()
+        drain()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -250,6 +279,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     e0.record(stream)
     for _ in range(args.steps):
         step()
+    drain()  # the last gathers are inside the timed region
     e1.record(stream)
     torch.cuda.synchronize()
     _lib.profile_enable(False)
@@ -507,6 +537,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--warmup-ref", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gather-overlap", action="store_true",
+                    help="N > 1: gather each step's XY before the next deskew instead of overlapping")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunk-frames", type=int, default=0)
     args = ap.parse_args()
