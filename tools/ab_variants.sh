@@ -11,7 +11,7 @@ for rep in 1 2; do
   for v in "$@"; do
     cp "variants/libssb_$v.so" paper_2211_00645_b200/lib/libssb.so
     echo "== $v (rep $rep)"
-    tools/time_variants.sh
+    ${TIMER:-tools/time_variants.sh}
   done
 done
 cp /tmp/libssb_orig.so paper_2211_00645_b200/lib/libssb.so
