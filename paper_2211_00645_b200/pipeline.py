@@ -359,9 +359,13 @@ class ProjectionCanvas:
         # rule yields the full re-max (ties keep the earliest slot)
         self._exact = True
         if self.mode == "rolling":
+            # the ring's frames are already resident: re-add each live slot's band from the
+            # device ring (no re-upload), in ring order, with the incremental rule
             for rf in self._ring:
                 if rf is not None:
-                    self.rolling_replace(rf)
+                    self._check_frame(rf)
+                    lo, hi = self.row_span(rf.slice_index)
+                    self._recompute_band(lo, hi, rf.slice_index)
 
 
 def deskew_place(canvas: ProjectionCanvas, frame: RawFrame) -> tuple[int, int]:
