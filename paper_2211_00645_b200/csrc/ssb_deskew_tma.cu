@@ -9,7 +9,8 @@
 //    global atomic counter -- big chunks first, a tail of short chunks last, u-tiles
 //    centre-out (heaviest first) -- and for every slice that touches the tile issues
 //    one 3-D TMA box load (256 columns x TU+2*slack frame rows, OOB zero-filled) into a
-//    5-stage (3 for 8-row tiles) shared-memory ring guarded by full/empty mbarriers;
+//    5-stage (3 for 8-row tiles) shared-memory ring guarded by full/empty mbarriers (the box
+//    load goes out as soon as a stage frees; the row table is built while it is in flight);
 //    its lanes also derive the per-row sampling table (fp64, once per row per slice);
 //  * consumer warp w owns 4 (or 8) canvas rows, lane l 8 columns: it reads the two
 //    taps of each canvas row from shared memory (conflict-free 512 B rows; chained
@@ -51,9 +52,9 @@ __host__ __device__ constexpr int box_slack() {
 }
 
 // Tile shape: 4 canvas rows per consumer warp (TU = 60, 5 stages) by default; projection-
-// only max mode (the live view, no volume to stream out) uses 8 rows (TU = 120, 3 stages),
-// amortising per-slice bookkeeping over twice the voxels.  Sum mode needs 8 u32
-// accumulators per row and always keeps 4 rows.
+// only max mode with XZ/YZ uses 8 rows (TU = 120, 3 stages), amortising the per-slice XZ
+// barrier and bookkeeping over twice the voxels.  Sum mode needs 8 u32 accumulators per row
+// and always keeps 4 rows.
 template <int ROWS>
 struct Cfg {
     static constexpr int kRows = ROWS;
