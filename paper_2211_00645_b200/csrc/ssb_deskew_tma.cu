@@ -873,10 +873,17 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     const bool clip = vol == nullptr && d.shear_px > 0.0 && env_i64("SSB_CLIP_SLICES", 1) != 0;
     const double span_slices = std::ceil((kTU + d.height + 4) / d.shear_px) + 2.0;
     const int64_t n_plan = clip && span_slices < (double)d.n ? (int64_t)span_slices : d.n;
-    int64_t n1 = n_plan * big_pct / 100;
+    // small problems (few pipeline stages per SM, e.g. config 1) pay a fixed cost per item
+    // (counter fetch, queue hand-off, pipeline fill): at most one item per ~16 stages of an SM's
+    // share, and no tail phase below ~64 stages per SM
+    const double stages_per_sm = (double)tiles * (double)n_plan / sms;
+    const int64_t per1 = std::max<int64_t>(
+        1, std::min<int64_t>(env_i64("SSB_ITEMS_PER_CTA", 2), (int64_t)(stages_per_sm / 16.0)));
+    const bool tail = stages_per_sm >= 64.0;
+    int64_t n1 = tail ? n_plan * big_pct / 100 : n_plan;
     if (n1 < 1) n1 = n_plan;
     int64_t S, chunk, S2, chunk2;
-    split(n1, env_i64("SSB_ITEMS_PER_CTA", 2), S, chunk);
+    split(n1, per1, S, chunk);
     split(n_plan - n1, env_i64("SSB_TAIL_ITEMS_PER_CTA", 6), S2, chunk2);
     const int64_t items = tiles * (S + S2);
     if (items > INT32_MAX / 2) return fail(SSB_ERR_CAPACITY, "too many tiles");

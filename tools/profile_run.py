@@ -16,6 +16,8 @@ ap.add_argument("--reduce", default="max")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--hw", type=int, default=2048)
+ap.add_argument("--h", type=int, default=0, help="frame rows (default: --hw)")
+ap.add_argument("--w", type=int, default=0, help="frame columns (default: --hw)")
 ap.add_argument("--no-volume", action="store_true")
 ap.add_argument("--formula", default="canvas")
 ap.add_argument("--axes", default="0,1,2")
@@ -24,7 +26,8 @@ a = ap.parse_args()
 axes = tuple(int(v) for v in a.axes.split(","))
 s = math.cos(math.radians(a.alpha))
 g = torch.Generator(device="cuda").manual_seed(1234)
-raw = torch.randint(0, 4096, (a.n, a.hw, a.hw), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
+fh, fw = a.h or a.hw, a.w or a.hw
+raw = torch.randint(0, 4096, (a.n, fh, fw), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
 res = None
 for _ in range(a.iters):
     res = deskew_device(raw, s, a.interp, reduce=a.reduce, formula=a.formula, write_volume=not a.no_volume,
