@@ -1,0 +1,41 @@
+"""bench.py's JSON contract, checked on CPU through the reference arm (no GPU needed).
+
+The driver parses one JSON line per run; the reference arm (`--impl reference`) times the
+reference algorithm's CPU port and must print the same keys as the GPU arm plus
+``impl`` / ``cpu_baseline`` / ``e2e``.  Ranks other than 0 print nothing and exit 0.
+"""
+import json
+import os
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(args, env=None):
+    e = dict(os.environ)
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), *args], capture_output=True, text=True,
+                          cwd=REPO, env=e, timeout=600)
+
+
+def test_reference_arm_prints_one_contract_line():
+    r = run(["--impl", "reference", "--config", "1", "--steps", "1", "--warmup", "1", "--ref-seconds", "1"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["warmup"] >= 3
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["workload"].startswith("config1")
+
+
+def test_reference_arm_nonzero_ranks_exit_quietly():
+    r = run(["--impl", "reference", "--config", "1", "--steps", "1", "--warmup", "1", "--ref-seconds", "1"],
+            env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert not [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
