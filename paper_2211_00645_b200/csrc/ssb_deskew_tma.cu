@@ -905,10 +905,19 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
         xz32 = static_cast<uint32_t *>(xz);
         yz32 = static_cast<uint32_t *>(yz);
     }
-    cudaMemsetAsync(counters, 0, sizeof(unsigned int), st);
-    if (xy32 && (mx || !acc)) cudaMemsetAsync(xy32, 0, n_xy * 4, st);
-    if (xz32) cudaMemsetAsync(xz32, 0, n_xz * 4, st);
-    if (yz32) cudaMemsetAsync(yz32, 0, n_yz * 4, st);
+    if (mx) {
+        // counter and the u32 scratch are contiguous in the workspace: one memset
+        char *end = reinterpret_cast<char *>(counters) + sizeof(unsigned int);
+        if (xy32) end = reinterpret_cast<char *>(xy32 + n_xy);
+        if (xz32) end = reinterpret_cast<char *>(xz32 + n_xz);
+        if (yz32) end = reinterpret_cast<char *>(yz32 + n_yz);
+        cudaMemsetAsync(counters, 0, (size_t)(end - reinterpret_cast<char *>(counters)), st);
+    } else {
+        cudaMemsetAsync(counters, 0, sizeof(unsigned int), st);
+        if (xy32 && !acc) cudaMemsetAsync(xy32, 0, n_xy * 4, st);
+        if (xz32) cudaMemsetAsync(xz32, 0, n_xz * 4, st);
+        if (yz32) cudaMemsetAsync(yz32, 0, n_yz * 4, st);
+    }
     if (int rc = check_launch("ssb_deskew scratch reset")) return rc;
 
     Params prm{};
