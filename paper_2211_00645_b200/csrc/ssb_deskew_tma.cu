@@ -257,6 +257,28 @@ __device__ __forceinline__ uint32_t lerp_one(const double a, const double b, con
     return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(tap_prod<C>(c0, a, n0), tap_prod<C>(c1, b, n1)), kRintMagic));
 }
 
+// np.interp with dx == 1 (phantom.reference_deskew, ss/phantom.py:396-402) from converted
+// taps: slope = b - a exactly, v = rint(fl(fl(slope * t) + a)); biased taps are unbiased by an
+// exact subtraction (their difference is exact either way)
+template <int C>
+__device__ __forceinline__ uint32_t np_one(const double a, const double b, const double t) {
+    const double av = native_tap<C>() ? a : __dsub_rn(a, kTwo52);
+    const double prod = __dmul_rn(__dsub_rn(b, a), t);  // == sign(d) * fl(|d| * t)
+    return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(prod, av), kRintMagic));
+}
+
+__device__ __forceinline__ void np_biased8_raw(const double (&a)[8], const double (&b)[8], const double t,
+                                               uint32_t (&r)[8]) {
+    r[0] = np_one<0>(a[0], b[0], t);
+    r[1] = np_one<1>(a[1], b[1], t);
+    r[2] = np_one<2>(a[2], b[2], t);
+    r[3] = np_one<3>(a[3], b[3], t);
+    r[4] = np_one<4>(a[4], b[4], t);
+    r[5] = np_one<5>(a[5], b[5], t);
+    r[6] = np_one<6>(a[6], b[6], t);
+    r[7] = np_one<7>(a[7], b[7], t);
+}
+
 __device__ __forceinline__ void lerp_biased8_raw(const double (&a)[8], const double (&b)[8], const double c0,
                                                  const double c1, const double n0, const double n1,
                                                  uint32_t (&r)[8]) {
@@ -371,7 +393,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     constexpr bool kPairXz = kMax && SIDE && kStream;   // XZ over row pairs with 3-input maxes
     uint4 xz_prev = make_uint4(0, 0, 0, 0);
     const bool store = vrow != nullptr;
-    constexpr bool chain = CHAIN && INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS;
+    constexpr bool chain = CHAIN && INTERP == SSB_INTERP_LINEAR;
     auto consume = [&](const int k, const uint4 v) {
         if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, v);
         if (kMax) {
@@ -412,10 +434,11 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
             // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
             double cur[8];
             to_biased8(lds128(rg[k].off_b + lane_off), cur);
+            uint32_t r[8];
+            if (FORMULA == SSB_FORMULA_NPINTERP) np_biased8_raw(prev, cur, rg[k].c0, r);
+            else lerp_biased8_raw(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1, r);
             if (!kMax && kStream) {
                 // sums take the rounded voxels straight from the rint trick (no unpacking)
-                uint32_t r[8];
-                lerp_biased8_raw(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1, r);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) prev[c] = cur[c];
                 if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, pack8(r));
@@ -431,7 +454,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                 if (SIDE) yzv[k] = redux_add(rs);
                 continue;
             }
-            v = lerp_biased8(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1);
+            v = pack8(r);
 #pragma unroll
             for (int c = 0; c < 8; ++c) prev[c] = cur[c];
         } else {
@@ -542,11 +565,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int r0 = lane * ROWS;  // ROWS divides 32: a warp's rows share one word
                     const uint32_t bits = (live[r0 / 32] >> (r0 % 32)) & ((1u << ROWS) - 1);
                     any = bits != 0;
-                    if (INTERP == SSB_INTERP_LINEAR && FORMULA == SSB_FORMULA_CANVAS && bits == (1u << ROWS) - 1) {
+                    if (INTERP == SSB_INTERP_LINEAR && bits == (1u << ROWS) - 1) {
                         const RowP *g = &sm.rows[stage][r0];
                         chained = true;
 #pragma unroll
                         for (int k = 0; k + 1 < ROWS; ++k) chained &= g[k].off_b == g[k + 1].off_a;
+                        if (FORMULA == SSB_FORMULA_NPINTERP) {  // np.interp: dx == 1 rows only
+#pragma unroll
+                            for (int k = 0; k < ROWS; ++k) chained &= g[k].kind == 3;
+                        }
                     }
                 }
                 const uint32_t any_mask = __ballot_sync(0xffffffffu, any);
