@@ -24,6 +24,7 @@ from __future__ import annotations
 import time
 from collections import deque
 
+import numpy as np
 import torch
 
 from .errors import ParameterError
@@ -50,7 +51,7 @@ class ChannelDeskewer:
         n = geom.slice_count
         self.frame_ts: deque = deque(maxlen=n + 1)
         self._sweep_events: list = []        # (start, end) per placement of the current sweep
-        self._frame_proc: deque = deque(maxlen=n)   # rolling: per-refresh (start, end) / ms
+        self._frame_proc_ms: deque = deque(maxlen=n)  # rolling: device ms of the last N refreshes
         self._frame_plot_ms: deque = deque(maxlen=n)
 
     # -- parameters (ss/pipeline.py:850-871, applied at a frame boundary) -------------------
@@ -118,17 +119,30 @@ class ChannelDeskewer:
             _, ev = self._timed(lambda: self.canvas.rolling_replace(frame))
             with torch.cuda.stream(self.stream):
                 projection = self.canvas.max_pixels_device.clone()
-            self._frame_proc.append(ev)
-            proc_events = list(self._frame_proc)
+            proc_events = [ev]
         image, pev = self._timed(lambda: warp_projection_device(projection, self.vt.warp_scale, self.stream))
         pev[1].synchronize()
+        # each event pair is read once (an elapsed_time call per pair); rolling mode keeps the
+        # last N refreshes as numbers, as the reference keeps its per-exposure durations
         processing_ms = sum(a.elapsed_time(b) for a, b in proc_events)
         if self.mode == "rolling":
+            self._frame_proc_ms.append(processing_ms)
+            processing_ms = sum(self._frame_proc_ms)
             self._frame_plot_ms.append(pev[0].elapsed_time(pev[1]))
             plotting_ms = sum(self._frame_plot_ms)
         else:
             plotting_ms = pev[0].elapsed_time(pev[1])
-        pixels = image if self.device_pixels else image.cpu().numpy()
+        if self.device_pixels:
+            pixels = image
+        else:
+            # page-locked landing buffer (cached by torch's host allocator), owned by the image
+            host = torch.empty(tuple(image.shape), dtype=torch.int16, pin_memory=True)
+            host.copy_(image.view(torch.int16), non_blocking=True)
+            torch.cuda.current_stream(image.device).wait_stream(self.stream)
+            host_done = torch.cuda.Event()
+            host_done.record(self.stream)
+            host_done.synchronize()
+            pixels = host.numpy().view(np.uint16)
         t1 = self.clock_ns()
         timings = StageTimings(acquisition_ms=self.stack_period_ms(), processing_ms=processing_ms,
                                plotting_ms=plotting_ms, lag_ms=max(0.0, (t1 - frame.timestamp_ns) / 1e6))

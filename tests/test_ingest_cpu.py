@@ -54,3 +54,26 @@ def test_truncated_raw_rejected(tmp_path):
     shutil.copy(os.path.join(FILES, "stack.json"), tmp_path / "t.json")
     with pytest.raises(MetadataError, match="not a multiple"):
         load_stack(raw, pinned=False)
+
+
+@pytest.mark.parametrize("name", ["stack.raw", "stack.tif"])
+def test_reads_into_a_caller_buffer(name):
+    want = np.load(os.path.join(FILES, "frames.npy"))
+    buf = np.full(want.shape, 7, dtype=np.uint16)
+    stack, _, _ = load_stack(os.path.join(FILES, name), out=buf)
+    assert stack is buf
+    np.testing.assert_array_equal(buf, want)
+    with pytest.raises(MetadataError, match="out buffer"):
+        load_stack(os.path.join(FILES, name), out=np.zeros((5, 10, 24), np.uint16))
+
+
+def test_parallel_raw_read_in_small_pieces(tmp_path):
+    # many pieces and a ragged last piece go to the right offsets
+    from paper_2211_00645_b200.ingest import _read_parallel
+
+    data = np.random.default_rng(3).integers(0, 256, 1_000_003, dtype=np.uint8)
+    path = tmp_path / "blob.bin"
+    data.tofile(path)
+    out = np.zeros_like(data)
+    _read_parallel(str(path), memoryview(out), data.size, threads=4, piece=4099)
+    np.testing.assert_array_equal(out, data)
