@@ -335,7 +335,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if not args.no_e2e:
         host = pinned_stack(n, h, w)
         host[:] = raw.cpu().numpy()
-        streamer = StackStreamer(h, w, device=dev)
+        streamer = StackStreamer(h, w, device=dev, chunk_frames=args.chunk_frames or None)
         out_host = {a: torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True) for a, t in projs.items()}
         # outputs stay allocated across steps, as in a running acquisition (no per-stack
         # allocation in the loop; the volume stays in HBM)
@@ -380,7 +380,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         h2d = 2 * n * h * w
         e2e = {"value": world * vox / (e_ms * 1e-3) / 1e9, "unit": "GVoxels/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in projs.values()),
-               "ms_per_step": e_ms, "h2d_gbs": h2d / (e_ms * 1e-3) / 1e9, "h2d_copy_ceiling_gbs": ceiling,
+               "ms_per_step": e_ms, "h2d_gbs": h2d / (e_ms * 1e-3) / 1e9, "h2d_copy_ceiling_gbs": ceiling, "chunk_frames": streamer.chunk,
                "path": "stream.StackStreamer.run (pinned host -> 2 copy streams -> ssb_deskew per chunk) + projections D2H; volume stays in HBM"}
 
     cpu = None
@@ -471,7 +471,7 @@ def run_stream(args, cfg, rank, world, local_rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 in / f64 lerp / u16 out",
             "data": "synthetic uniform [0,4096) in pinned host memory",
             "config": {"workload": cfg["name"], "interp": args.interp, "canvas": [u, w], "stacks_per_s": 1e3 / ms,
-                       "latency_ms_last_chunk_to_host": lat, "chunk_frames": streamer.chunk,
+                       "latency_ms_last_chunk_to_host": lat, "chunk_frames": streamer.chunk, "tail_frames": streamer.tail,
                        "outputs": "XY/XZ/YZ max to host every stack, no volume",
                        "h2d_GBps": 2 * n * h * w / (ms * 1e-3) / 1e9},
             "gpu_launches": launches,
@@ -483,7 +483,7 @@ def run_slabs(args, cfg, rank, world, local_rank):
 
     Rank r deskews frames [first, first+count) with global slice indices over its canvas
     row window, projection-only, sum XY (uint32); the partial canvases are merged on rank 0
-    with one NCCL reduce (int64 sum) inside the timed step.
+    with one NCCL reduce (uint32 bits as int32 sum) inside the timed step.
     """
     import torch
     import torch.distributed as dist

@@ -15,8 +15,10 @@ per GPU over ``torch.distributed`` (NCCL on B200, gloo in the CPU tests):
   projections are merged on the display rank: XY by an element-wise reduce
   (max or sum) of the row windows, XZ / YZ by concatenation along the slice axis.
 
-NCCL has no uint16 type, so uint16 maxima travel widened to int32; uint32 sums
-travel as int64.
+NCCL has no uint16 type, so uint16 maxima travel widened to int32.  uint32 sums
+travel bit-cast as int32: two's-complement addition is the same bit operation as
+uint32 addition, so the int32 SUM is exactly the uint32 sum (mod 2^32, like the
+single-GPU kernel's u32 reduction) at half the bytes of an int64 widening.
 """
 
 from __future__ import annotations
@@ -81,8 +83,12 @@ def deskew_slab(raw_slab: torch.Tensor, plan: SlabPlan, shear_px: float, interp:
 
 
 def _wide(t: torch.Tensor, reduce: str) -> torch.Tensor:
-    """Widen uint16 / uint32 projection values to an NCCL-reducible integer type."""
-    return t.to(torch.int32) if reduce == "max" else t.to(torch.int64)
+    """uint16 maxima widened to int32; uint32 sums bit-cast to int32 (same bits)."""
+    return t.to(torch.int32) if reduce == "max" else t.contiguous().view(torch.int32)
+
+
+def _narrow(t: torch.Tensor, reduce: str) -> torch.Tensor:
+    return t.to(torch.uint16) if reduce == "max" else t.view(torch.uint32)
 
 
 def combine_xy(partial: torch.Tensor, plan: SlabPlan, width: int, reduce: str = "sum", dst: int = 0,
@@ -94,15 +100,14 @@ def combine_xy(partial: torch.Tensor, plan: SlabPlan, width: int, reduce: str = 
     neutral for both reductions.  Returns the canvas on ``dst`` (uint16 for max,
     uint32 for sum), None elsewhere.
     """
-    full = torch.zeros((plan.canvas_rows, width), dtype=torch.int32 if reduce == "max" else torch.int64,
-                       device=partial.device)
+    full = torch.zeros((plan.canvas_rows, width), dtype=torch.int32, device=partial.device)
     if plan.count:
         full[plan.u_begin:plan.u_begin + plan.u_count] = _wide(partial, reduce)
     op = dist.ReduceOp.MAX if reduce == "max" else dist.ReduceOp.SUM
     dist.reduce(full, dst=dst, op=op, group=group)
     if dist.get_rank(group) != dst:
         return None
-    return full.to(torch.uint16) if reduce == "max" else full.to(torch.uint32)
+    return _narrow(full, reduce)
 
 
 def gather_slices(partial: torch.Tensor, plans: list, rank: int, length: int, reduce: str = "sum",
@@ -114,8 +119,7 @@ def gather_slices(partial: torch.Tensor, plans: list, rank: int, length: int, re
     """
     plan = plans[rank]
     rows = max(p.count for p in plans)
-    buf = torch.zeros((rows, length), dtype=torch.int32 if reduce == "max" else torch.int64,
-                      device=partial.device)
+    buf = torch.zeros((rows, length), dtype=torch.int32, device=partial.device)
     if plan.count:
         if window:
             buf[:plan.count, plan.u_begin:plan.u_begin + plan.u_count] = _wide(partial, reduce)
@@ -126,7 +130,7 @@ def gather_slices(partial: torch.Tensor, plans: list, rank: int, length: int, re
     if bufs is None:
         return None
     out = torch.cat([b[:p.count] for b, p in zip(bufs, plans)])
-    return out.to(torch.uint16) if reduce == "max" else out.to(torch.uint32)
+    return _narrow(out.contiguous(), reduce)
 
 
 def gather_to_display(projection: torch.Tensor, dst: int = 0, group=None):

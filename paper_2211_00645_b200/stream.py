@@ -49,6 +49,15 @@ def _as_host_tensor(stack) -> torch.Tensor:
     return torch.from_numpy(arr)
 
 
+def chunk_bounds(n: int, chunk: int, tail: int) -> list:
+    """[c0, c1) frame ranges: full chunks, the last one split so it holds <= ``tail`` frames."""
+    bounds = [(c0, min(n, c0 + chunk)) for c0 in range(0, n, chunk)]
+    if bounds and bounds[-1][1] - bounds[-1][0] > tail:
+        c0, c1 = bounds.pop()
+        bounds += [(c0, c1 - tail), (c1 - tail, c1)]
+    return bounds
+
+
 @dataclass
 class StreamTimings:
     """Host-side wall times of the last run (ms)."""
@@ -61,13 +70,20 @@ class StackStreamer:
     """Chunked H2D + deskew pipeline for one frame geometry (H, W)."""
 
     def __init__(self, height: int, width: int, *, chunk_frames: int | None = None,
-                 n_buffers: int = 3, device: torch.device | None = None):
+                 tail_frames: int | None = None, n_buffers: int = 3, device: torch.device | None = None):
         self.device = device or require_cuda()
         self.height, self.width = int(height), int(width)
         frame_bytes = 2 * self.height * self.width
         if chunk_frames is None:
-            chunk_frames = max(1, (256 << 20) // frame_bytes)
+            # 64 MB chunks: measured on B200 (config 3, 200 x 1024^2): 16-64 MB chunks keep the
+            # PCIe link saturated (7.65 ms/stack), 128-256 MB chunks stall it (11-13.6 ms)
+            chunk_frames = max(1, (64 << 20) // frame_bytes)
+        if tail_frames is None:
+            # the last chunk is cut to <= 16 MB: it is the one whose copy + deskew + D2H is the
+            # live view's latency (last frame on the host -> projections on the host)
+            tail_frames = max(1, (16 << 20) // frame_bytes)
         self.chunk = int(chunk_frames)
+        self.tail = max(1, min(int(tail_frames), self.chunk))
         self.n_buffers = max(2, int(n_buffers))
         shape = (self.chunk, self.height, self.width)
         self.dev_bufs = [torch.empty(shape, dtype=torch.uint16, device=self.device)
@@ -80,6 +96,9 @@ class StackStreamer:
         #: if set to a timing-enabled torch.cuda.Event, run() records it on the copy stream
         #: right before the last chunk's H2D copy (end-to-end latency measurement)
         self.last_chunk_event = None
+
+    def chunk_bounds(self, n: int) -> list:
+        return chunk_bounds(n, self.chunk, self.tail)
 
     def _staging_ring(self):
         if self._staging is None:
@@ -114,10 +133,10 @@ class StackStreamer:
                 projs = {a: torch.empty(shapes[a], dtype=pdt, device=dev) for a in axes}
             else:
                 volume, projs = out.volume, dict(out.projections)
-        n_chunks = (n + self.chunk - 1) // self.chunk
-        for c in range(n_chunks):
+        bounds = self.chunk_bounds(n)
+        n_chunks = len(bounds)
+        for c, (c0, c1) in enumerate(bounds):
             b = c % self.n_buffers
-            c0, c1 = c * self.chunk, min(n, (c + 1) * self.chunk)
             m = c1 - c0
             cs = self.copy_streams[c % 2]
             if self._done[b] is not None:

@@ -89,3 +89,35 @@ def test_uneven_and_empty_slabs():
     plans = D.plan_slabs(3, 4, 1.0, "nearest", 5)
     assert [p.count for p in plans] == [1, 1, 1, 0, 0]
     assert D.shard_stacks(64, 3, 8) == [3, 11, 19, 27, 35, 43, 51, 59]
+
+
+def _wrap_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plans = D.plan_slabs(4, 3, 1.0, "nearest", world)  # canvas rows 6
+        p = plans[rank]
+        part = np.full((p.u_count, 5), 0xFFFFFFF0 + rank, dtype=np.uint32)
+        part[0, 0] = 7
+        xy = D.combine_xy(torch.from_numpy(part), p, 5, "sum")
+        if rank == 0:
+            np.save(os.path.join(out_dir, "xy.npy"), xy.numpy())
+            np.save(os.path.join(out_dir, "plans.npy"), np.array([[q.u_begin, q.u_count] for q in plans]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sum_combine_wraps_like_uint32(tmp_path):
+    """uint32 sums travel bit-cast as int32: the merge equals uint32 addition mod 2^32."""
+    mp.start_processes(_wrap_worker, args=(WORLD, free_port(), str(tmp_path)), nprocs=WORLD, join=True,
+                       start_method="spawn")
+    got = np.load(tmp_path / "xy.npy")
+    plans = np.load(tmp_path / "plans.npy")
+    want = np.zeros((6, 5), dtype=np.uint64)
+    for r, (b, c) in enumerate(plans):
+        part = np.full((c, 5), 0xFFFFFFF0 + r, dtype=np.uint64)
+        part[0, 0] = 7
+        want[b:b + c] += part
+    assert got.dtype == np.uint32
+    np.testing.assert_array_equal(got, (want % (1 << 32)).astype(np.uint32))
+    assert (want >= (1 << 32)).any()  # the case really wraps

@@ -367,7 +367,7 @@ def test_streamer_chunks_match_single_launch(kernel_path):
     pin[:] = st
     for src in (st, pin):
         for reduce in ("max", "sum"):
-            streamer = StackStreamer(h, w, chunk_frames=5)
+            streamer = StackStreamer(h, w, chunk_frames=5, tail_frames=2 if reduce == "max" else None)
             res = streamer.run(src, s, "linear", reduce=reduce)
             torch.cuda.synchronize()
             _, want_r = C.deskew(st, s, "linear", reduce=reduce)

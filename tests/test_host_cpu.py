@@ -107,3 +107,27 @@ class TestNoCpuFallback:
     def test_warp_needs_device(self):
         with pytest.raises(DeviceError):
             pl.warp_projection(np.zeros((4, 2), np.uint16), 1.5)
+
+
+class TestChunkBounds:
+    """Chunking of the pinned H2D pipeline: full chunks, then a short last chunk (latency)."""
+
+    def test_cover_in_order(self):
+        from paper_2211_00645_b200.stream import chunk_bounds
+        for n in (1, 7, 8, 9, 31, 32, 33, 200):
+            for chunk in (1, 4, 32):
+                for tail in (1, 2, 8):
+                    b = chunk_bounds(n, chunk, min(tail, chunk))
+                    assert b[0][0] == 0 and b[-1][1] == n
+                    assert all(c1 > c0 for c0, c1 in b)
+                    assert all(b[k][1] == b[k + 1][0] for k in range(len(b) - 1))
+                    assert max(c1 - c0 for c0, c1 in b) <= chunk
+                    assert b[-1][1] - b[-1][0] <= min(tail, chunk)
+
+    def test_config3_shape(self):
+        from paper_2211_00645_b200.stream import chunk_bounds
+        # 200 frames of 1024^2: 64 MB chunks (32 frames), <= 16 MB (8 frames) last
+        b = chunk_bounds(200, 32, 8)
+        assert b[-1] == (192, 200) and len(b) == 7
+        b = chunk_bounds(64, 32, 8)
+        assert b == [(0, 32), (32, 56), (56, 64)]
