@@ -194,7 +194,27 @@ def run_reference(args, cfg, rank, world):
                          "sample": det["sample"]},
         "e2e": {"value": gv, "unit": "GVoxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if n * u * w <= (64 << 20):
+        # small stacks (config 1): also the reference's batch oracle as-is (fp64 pile, one
+        # np.interp per column, ss/phantom.py:359-402), single process
+        line["reference_deskew_as_is"] = reference_deskew_as_is_timing(cfg, interp)
     print(json.dumps(line), flush=True)
+
+
+def reference_deskew_as_is_timing(cfg, interp, reps=3):
+    from oracle import deskew_oracle as O
+
+    n, h, w = cfg["n"], cfg["h"], cfg["w"]
+    s = native_shear(cfg["alpha"])
+    stack = np.random.default_rng(0).integers(0, 4096, size=(n, h, w)).astype(np.uint16)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.reference_deskew_as_is(stack, s, interp)
+        ts.append(time.perf_counter() - t0)
+    ms = sorted(ts)[len(ts) // 2] * 1e3
+    return {"ms_per_stack": ms, "cores": 1, "interp": interp,
+            "what": "oracle.reference_deskew_as_is: (n,U,W) fp64 pile, np.interp per column, max/rint/clip"}
 
 
 def run_ours(args, cfg, rank, world, local_rank):
@@ -304,6 +324,24 @@ def run_ours(args, cfg, rank, world, local_rank):
         ms = sum(a0.elapsed_time(a1) for a0, a1 in pairs) / args.steps
     l2_note = ("inputs %.2f GB and outputs %.2f GB >> 126 MB L2; no flush" % (2 * n * h * w / 1e9, 2 * n * u * w / 1e9)
                if flush is None else "L2 flushed (512 MB write) before each step; steps timed individually")
+    batch = None
+    if flush is not None:
+        # small stacks (config 1): the reference's batch oracle (reference_deskew: np.interp rows,
+        # pile max, ss/phantom.py:359-402) on the device, XY only, L2 flushed before each call
+        pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(args.steps)]
+        xy_b = torch.empty((u, w), dtype=torch.uint16, device=dev)
+        for a0, a1 in pairs:
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            a0.record(stream)
+            deskew_device(raw, s, interp, formula="npinterp", projection_axes=(0,), write_volume=False,
+                          projections={0: xy_b}, stream=stream)
+            a1.record(stream)
+        torch.cuda.synchronize()
+        bt = sorted(a0.elapsed_time(a1) for a0, a1 in pairs)
+        batch = {"ms_per_stack": bt[len(bt) // 2], "what": "phantom.reference_deskew formula (SSB_FORMULA_NPINTERP), "
+                 "XY max only, device-resident stack, L2 flushed before each call"}
     del flush
     _lib.profile_enable(False)
     kern_ms, kern_n = _lib.profile_read()
@@ -405,6 +443,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                          "kernel": "deskew_tma_kernel (TMA-pipelined persistent)"},
             "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
         }
+        if batch is not None:
+            line["reference_deskew_gpu"] = batch
         print(json.dumps(line), flush=True)
 
 

@@ -201,6 +201,33 @@ def reference_deskew(stack, shear: float, interp: str = "nearest") -> np.ndarray
     return np.clip(np.rint(out), 0, MAX_INTENSITY).astype(np.uint16)
 
 
+def reference_deskew_as_is(stack, shear: float, interp: str = "linear") -> np.ndarray:
+    """ss/phantom.py:359-402 with the reference's own cost structure, for CPU timing only.
+
+    Same result as ``reference_deskew``, but built the way the reference builds it: an
+    (n, U, W) float64 pile of per-slice canvases (ss/phantom.py:390), one ``np.interp``
+    call per frame column for linear slices (ss/phantom.py:396-400), then one max over the
+    pile, rint and clip (ss/phantom.py:401-402).  ``bench.py --impl reference --config 1``
+    times it beside the streaming path.
+    """
+    stack = np.asarray(stack)
+    n, h, w = stack.shape
+    pile = np.zeros((n, canvas_height(n, h, shear), w), dtype=np.float64)
+    rows_in_frame = np.arange(h)
+    for i in range(n):
+        frame = stack[i]
+        if interp == "nearest":
+            top = nearest_offset(i, shear)
+            pile[i, top:top + h] = frame
+            continue
+        lo, hi = linear_span(i, shear, h)
+        targets = np.arange(lo, hi + 1, dtype=np.float64)
+        sample_at = i * shear + rows_in_frame
+        for col in range(w):
+            pile[i, lo:hi + 1, col] = np.interp(targets, sample_at, frame[:, col].astype(np.float64))
+    return np.clip(np.rint(pile.max(axis=0)), 0, MAX_INTENSITY).astype(np.uint16)
+
+
 # ---------------------------------------------------------------------------
 # display warp and rolling mode
 

@@ -868,7 +868,8 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     const bool side = xz != nullptr || yz != nullptr;
     // 8-row tiles pay only where the per-row XZ/YZ work dominates: projection-only max with side
     // projections (measured: XY-only is faster with 4-row tiles and their deeper 5-stage ring)
-    const bool tall = vol == nullptr && env_i64("SSB_TALL_TILES", 1) != 0 && mx && side;
+    const int64_t tall_env = env_i64("SSB_TALL_TILES", 1);  // 0 never, 1 projection-only, 2 always (A/B)
+    const bool tall = (vol == nullptr || tall_env == 2) && tall_env != 0 && mx && side;
     const int kTU = tall ? Cfg<8>::kTU : Cfg<4>::kTU;
     const int slack = d.interp == SSB_INTERP_NEAREST ? box_slack<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
                       : d.formula == SSB_FORMULA_CANVAS ? box_slack<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>()

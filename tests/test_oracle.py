@@ -23,6 +23,8 @@ def test_numpy_oracle_matches_reference_rows(case):
     bvol = O.deskew_volume(st, s, interp, "npinterp")
     np.testing.assert_array_equal(bvol, case["batch_vol"])
     np.testing.assert_array_equal(O.reference_deskew(st, s, interp), case["batch_xy"])
+    # the as-is port (pile + np.interp per column) the CPU arm times at config 1
+    np.testing.assert_array_equal(O.reference_deskew_as_is(st, s, interp), case["batch_xy"])
     np.testing.assert_array_equal(bvol.max(0), case["batch_xy"])
 
 
