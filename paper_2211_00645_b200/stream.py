@@ -30,12 +30,7 @@ def pinned_stack(n: int, height: int, width: int) -> np.ndarray:
     """(n, H, W) uint16 numpy array backed by page-locked host memory."""
     require_cuda()
     t = torch.empty((n, height, width), dtype=torch.uint16, pin_memory=True)
-    arr = t.numpy()
-    _PINNED_KEEPALIVE[arr.__array_interface__["data"][0]] = t
-    return arr
-
-
-_PINNED_KEEPALIVE: dict = {}
+    return t.numpy()  # the array's base holds the tensor: the pinned block lives as long as the array
 
 
 def _as_host_tensor(stack) -> torch.Tensor:
