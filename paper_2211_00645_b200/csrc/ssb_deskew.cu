@@ -47,29 +47,53 @@ struct TileParams {
     int32_t xy_accumulate;
 };
 
-template <bool VEC>
+// 8 consecutive uint16 per lane.  VB = widest access the buffers' alignment allows (16, 8, 4 or
+// 2 bytes): W % 8 == 0 stacks take 16-byte vectors, W % 4 == 0 (e.g. 4-pixel camera ROI steps) two
+// 8-byte halves, even W four 4-byte words; lanes that straddle the row end go element by element.
+template <int VB>
 __device__ __forceinline__ uint4 load8(const uint16_t *row, int64_t x, int64_t w) {
-    if (VEC) return ldg_nc_v4(row + x);
+    if (VB == 16) return ldg_nc_v4(row + x);
     uint32_t v[4] = {0, 0, 0, 0};
+    if (VB > 2 && x + 8 <= w) {
+        if (VB == 8) {
+            const uint2 a = __ldg(reinterpret_cast<const uint2 *>(row + x));
+            const uint2 b = __ldg(reinterpret_cast<const uint2 *>(row + x + 4));
+            return make_uint4(a.x, a.y, b.x, b.y);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = __ldg(reinterpret_cast<const uint32_t *>(row + x + 2 * q));
+        return make_uint4(v[0], v[1], v[2], v[3]);
+    }
 #pragma unroll
     for (int c = 0; c < 8; ++c)
         if (x + c < w) v[c >> 1] |= (uint32_t)__ldg(row + x + c) << (16 * (c & 1));
     return make_uint4(v[0], v[1], v[2], v[3]);
 }
 
-template <bool VEC>
+template <int VB>
 __device__ __forceinline__ void store8(uint16_t *row, int64_t x, int64_t w, uint4 v) {
-    if (VEC) {
+    if (VB == 16) {
         stg_cs_v4(row + x, v);
         return;
     }
     const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+    if (VB > 2 && x + 8 <= w) {
+        if (VB == 8) {
+            asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(row + x), "r"(q[0]), "r"(q[1]) : "memory");
+            asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(row + x + 4), "r"(q[2]), "r"(q[3]) : "memory");
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(row + x + 2 * k), "r"(q[k]) : "memory");
+        }
+        return;
+    }
 #pragma unroll
     for (int c = 0; c < 8; ++c)
         if (x + c < w) row[x + c] = (uint16_t)(q[c >> 1] >> (16 * (c & 1)));
 }
 
-template <int ROWS, int INTERP, int FORMULA, int REDUCE, bool VEC>
+template <int ROWS, int INTERP, int FORMULA, int REDUCE, int VEC>
 __global__ void __launch_bounds__(kThreads) deskew_tiles_kernel(const TileParams p) {
     constexpr int TU = kWarps * ROWS;
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
@@ -296,13 +320,16 @@ int validate(const ssb_deskew_desc *d) {
 }
 
 template <int ROWS, int INTERP, int FORMULA, int REDUCE>
-void launch_tiles(const TileParams &tp, int64_t items, bool vec, cudaStream_t st) {
-    if (vec) deskew_tiles_kernel<ROWS, INTERP, FORMULA, REDUCE, true><<<(unsigned)items, kThreads, 0, st>>>(tp);
-    else deskew_tiles_kernel<ROWS, INTERP, FORMULA, REDUCE, false><<<(unsigned)items, kThreads, 0, st>>>(tp);
+void launch_tiles(const TileParams &tp, int64_t items, int vec, cudaStream_t st) {
+    const unsigned g = (unsigned)items;
+    if (vec == 16) deskew_tiles_kernel<ROWS, INTERP, FORMULA, REDUCE, 16><<<g, kThreads, 0, st>>>(tp);
+    else if (vec == 8) deskew_tiles_kernel<ROWS, INTERP, FORMULA, REDUCE, 8><<<g, kThreads, 0, st>>>(tp);
+    else if (vec == 4) deskew_tiles_kernel<ROWS, INTERP, FORMULA, REDUCE, 4><<<g, kThreads, 0, st>>>(tp);
+    else deskew_tiles_kernel<ROWS, INTERP, FORMULA, REDUCE, 2><<<g, kThreads, 0, st>>>(tp);
 }
 
 template <int REDUCE>
-void dispatch_interp(const ssb_deskew_desc &d, const TileParams &tp, int64_t items, bool vec,
+void dispatch_interp(const ssb_deskew_desc &d, const TileParams &tp, int64_t items, int vec,
                      cudaStream_t st) {
     constexpr int R = REDUCE == SSB_REDUCE_MAX ? 8 : 4;
     if (d.interp == SSB_INTERP_NEAREST)
@@ -387,9 +414,15 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
         tp.XT = (int32_t)pl.XT;
         tp.S = (int32_t)pl.S;
         tp.xy_accumulate = xy_acc;
-        const bool vec = (d->width % 8 == 0) && (tp.row_stride % 8 == 0) && (tp.frame_stride % 8 == 0) &&
-                         aligned16(raw) && aligned16(vol) &&
-                         (d->reduce != SSB_REDUCE_MAX || aligned16(tp.xy));
+        // widest access every buffer's alignment allows (element strides and base addresses)
+        auto fits = [&](int vb) {
+            const int64_t e = vb / 2;
+            const uintptr_t m = (uintptr_t)vb - 1;
+            return d->width % e == 0 && tp.row_stride % e == 0 && tp.frame_stride % e == 0 &&
+                   ((uintptr_t)raw & m) == 0 && ((uintptr_t)vol & m) == 0 &&
+                   (d->reduce != SSB_REDUCE_MAX || ((uintptr_t)tp.xy & m) == 0);
+        };
+        const int vec = fits(16) ? 16 : fits(8) ? 8 : fits(4) ? 4 : 2;
         const int64_t items = pl.UT * pl.XT * pl.S;
         if (items > INT32_MAX) return fail(SSB_ERR_CAPACITY, "too many tiles");
         profile_begin(st);

@@ -140,6 +140,7 @@ class ProjectionCanvas:
         self._present_dev = None   # (N,) uint8
         self._roll_ws = None       # device list of voxels to re-max (incremental rolling updates)
         self._host_cache = None
+        self._pending_uploads: list = []  # (copy-done event, pinned host buffer) still being read
         # True while canvas + contributor equal the full re-max over the ring, so a
         # rolling_replace can take the O(band) incremental path (see ssb_rolling_band)
         self._exact = True
@@ -167,9 +168,18 @@ class ProjectionCanvas:
             dev = host.to(self._device, non_blocking=pinned).unsqueeze(0)
         if pinned:
             # RawFrame pixels are immutable (ss/pipeline.py:37-39), so the copy may still be
-            # reading them after place() returns; hold a reference until the next upload
-            self._pending_upload = host
+            # reading them after place() returns: hold the host buffer until its copy completes
+            self._hold_until_copied(host)
         return dev
+
+    def _hold_until_copied(self, host: torch.Tensor) -> None:
+        """Keep a pinned host buffer alive until the asynchronous H2D copy just queued on the
+        canvas stream has read it (the caller may drop the frame as soon as place() returns)."""
+        done = torch.cuda.Event()
+        done.record(self.stream)
+        pending = [(e, h) for e, h in self._pending_uploads if not e.query()]
+        pending.append((done, host))
+        self._pending_uploads = pending
 
     @property
     def max_pixels(self) -> np.ndarray:
@@ -313,7 +323,7 @@ class ProjectionCanvas:
             self._ring_dev[frame.slice_index].copy_(host, non_blocking=pinned)
             self._present_dev[frame.slice_index] = 1
         if pinned:
-            self._pending_upload = host  # the async copy may still read it (see _upload)
+            self._hold_until_copied(host)  # the async copy may still read it (see _upload)
 
     def rolling_replace(self, frame: RawFrame) -> tuple[int, int]:
         """Swap in the newest version of a slice and refresh its band (ss/pipeline.py:345-359)."""

@@ -548,3 +548,45 @@ def test_projection_only_long_scans_and_slabs(seed):
         _, pr = run(st, s, interp, reduce=reduce, write_volume=False, projection_axes=(0, 1, 2))
         for ax in (0, 1, 2):
             np.testing.assert_array_equal(pr[ax], O.project(full_vol, ax, reduce))
+
+
+def test_place_from_transient_pinned_frames():
+    """place() copies pinned frames asynchronously; the canvas keeps each host buffer alive until
+    its copy completed, so callers may drop frames right away; the hold list stays bounded."""
+    from paper_2211_00645_b200.stream import pinned_stack
+
+    rng = np.random.default_rng(23)
+    n, h, w, s = 24, 64, 256, 0.8660254037844386
+    st = rng.integers(0, 65536, (n, h, w)).astype(np.uint16)
+    c = pl.ProjectionCanvas(geom(n=n, w=w, h=h), s, "linear")
+    for i in range(n):
+        buf = pinned_stack(1, h, w)[0]
+        buf[:] = st[i]
+        c.place(pl.RawFrame(buf, i))
+        del buf
+    np.testing.assert_array_equal(c.finalize_global(), O.canvas_max(st, s, "linear"))
+    torch.cuda.synchronize()
+    c.place(pl.RawFrame(pinned_stack(1, h, w)[0], 0))
+    assert len(c._pending_uploads) <= 2
+
+
+@pytest.mark.parametrize("w,offset", [(12, 0), (20, 2), (260, 0), (262, 0), (263, 0), (516, 4), (136, 6),
+                                      (136, 8), (1000, 0)])
+def test_generic_path_vector_widths(w, offset):
+    """Widths / base offsets that are not TMA-eligible pick the widest access their alignment
+    allows (8-, 4- or 2-byte); every one must stay bit-exact, straddling lanes included."""
+    rng = np.random.default_rng(w * 10 + offset)
+    n, h = 11, 37
+    st = rng.integers(0, 65536, (n, h, w)).astype(np.uint16)
+    e = offset // 2
+    buf = torch.empty(n * h * w + e, dtype=torch.uint16, device=dev())
+    buf[e:].copy_(torch.from_numpy(st.reshape(-1)).to(dev()))
+    raw = buf[e:].view(n, h, w)
+    for interp in ("linear", "nearest"):
+        for reduce in ("max", "sum"):
+            res = deskew_device(raw, 0.8660254037844386, interp, reduce=reduce)
+            torch.cuda.synchronize()
+            want_vol, want = C.deskew(st, 0.8660254037844386, interp, reduce=reduce)
+            np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
+            for ax in (0, 1, 2):
+                np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])

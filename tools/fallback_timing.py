@@ -10,7 +10,7 @@ import torch  # noqa: E402
 from paper_2211_00645_b200.deskew import deskew_device  # noqa: E402
 
 s = math.cos(math.radians(30.0))
-for w, disable in ((2048, "0"), (2048, "1"), (2044, "0")):
+for w, disable in ((2048, "0"), (2048, "1"), (2044, "0"), (2046, "0"), (2047, "0")):
     os.environ["SSB_DISABLE_TMA"] = disable
     raw = torch.randint(0, 4096, (512, 2048, w), dtype=torch.int32, device="cuda").to(torch.uint16)
     res = deskew_device(raw, s, "linear")
