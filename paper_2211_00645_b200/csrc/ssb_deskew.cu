@@ -380,8 +380,8 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
     // a handful of frames folded into XY only (ProjectionCanvas.place, ss/pipeline.py:316-323) is
     // one small launch of the tiled kernel: no scratch reset, no finalize pass
     const bool tiny = d->n <= 2 && xz == nullptr && yz == nullptr;
-    const bool use_tma = env_int("SSB_DISABLE_TMA", 0) == 0 && !tiny && tma_eligible(*d, raw, vol, xy);
-    if (use_tma) return launch_deskew_tma(*d, raw, vol, xy, xz, yz, workspace, workspace_bytes, st);
+    const int ac = (env_int("SSB_DISABLE_TMA", 0) == 0 && !tiny) ? persistent_access_class(*d, raw, vol, xy) : 0;
+    if (ac) return launch_deskew_tma(*d, raw, vol, xy, xz, yz, workspace, workspace_bytes, st, ac);
 
     const Plan pl = make_plan(*d, xy != nullptr, xz != nullptr, yz != nullptr, tiled_rows(*d), false);
     const size_t need = kCounterBytes + pl.xy_ws + pl.xz_ws + pl.yz_ws;

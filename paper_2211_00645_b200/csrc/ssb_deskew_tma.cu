@@ -99,13 +99,25 @@ struct Params {
     int32_t UT, XT, S, S2, n_items, xy_accumulate;
     int32_t clip;        // projection-only: each u-tile visits only the slices that can touch it
     int32_t big_pct;     // (clip) phase-1 share of a tile's slice range, percent
+    const uint16_t *raw;  // row-copy mode (AC < 16): frames and their element strides
+    int64_t row_stride, frame_stride;
 };
 
-template <int ROWS>
+// AC: 16 = rows reach shared memory through one 3-D TMA box (16-byte aligned rows);
+// 8 / 4 / 2 = row-copy mode for rows that are not 16-byte aligned (W % 8 != 0, offset crops): the
+// producer issues one 1-D bulk copy per frame row of the row's 16-byte-aligned superset into a
+// 528-byte slot, the row table points each tap at its first pixel inside the slot, and consumers
+// read / write 8 pixels with accesses of AC bytes (the widest every row's alignment allows).
+template <int AC>
+__host__ __device__ constexpr int row_pitch() {
+    return AC == 16 ? kTX : kTX + 8;
+}
+
+template <int ROWS, int AC = 16>
 struct Smem {
     using C = Cfg<ROWS>;
-    uint16_t box[C::kStages][C::kBoxRows][kTX];
-    uint16_t zero_row[kTX];
+    uint16_t box[C::kStages][C::kBoxRows][row_pitch<AC>()];
+    uint16_t zero_row[kTX + 8];
     RowP rows[C::kStages][C::kTU];
     uint32_t hdr[C::kStages];  // bit 16: slice touches the tile; bits 0..14: warps with live rows;
                                // bits 17..31: warps whose rows chain their taps
@@ -317,6 +329,76 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+
+// 8 pixels from shared memory at a 2-byte aligned address known to be AC-byte aligned
+template <int AC>
+__device__ __forceinline__ uint4 lds8(uint32_t a) {
+    if (AC == 16) return lds128(a);
+    if (AC == 8) {
+        const uint2 x = lds64(a), y = lds64(a + 8);
+        return make_uint4(x.x, x.y, y.x, y.y);
+    }
+    if (AC == 4) return make_uint4(lds32(a), lds32(a + 4), lds32(a + 8), lds32(a + 12));
+    // 2-byte aligned: five aligned words, shifted by 0 or 2 bytes (selector is warp-uniform per row)
+    const uint32_t b = a & ~3u, sel = (a & 2u) ? 0x5432u : 0x3210u;
+    const uint32_t w0 = lds32(b), w1 = lds32(b + 4), w2 = lds32(b + 8), w3 = lds32(b + 12), w4 = lds32(b + 16);
+    return make_uint4(__byte_perm(w0, w1, sel), __byte_perm(w1, w2, sel), __byte_perm(w2, w3, sel),
+                      __byte_perm(w3, w4, sel));
+}
+
+// 8 pixels to the volume (streaming stores) at an AC-byte aligned address
+template <int AC>
+__device__ __forceinline__ void stg8(uint16_t *p, const uint4 v) {
+    if (AC == 16) {
+        stg_cs_v4(p, v);
+    } else if (AC == 8) {
+        asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+        asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p + 4), "r"(v.z), "r"(v.w) : "memory");
+    } else if (AC == 4 || (reinterpret_cast<uintptr_t>(p) & 2u) == 0) {
+        const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + 2 * k), "r"(q[k]) : "memory");
+    } else {
+        // 2 mod 4: one pixel, three aligned words across pixel pairs, one pixel
+        asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"((unsigned short)(v.x & 0xFFFFu)) : "memory");
+        asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + 1), "r"(__byte_perm(v.x, v.y, 0x5432)) : "memory");
+        asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + 3), "r"(__byte_perm(v.y, v.z, 0x5432)) : "memory");
+        asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + 5), "r"(__byte_perm(v.z, v.w, 0x5432)) : "memory");
+        asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p + 7), "h"((unsigned short)(v.w >> 16)) : "memory");
+    }
+}
+
+// the first nv (< 8) pixels of a lane that straddles the right edge (row-copy mode only)
+__device__ __forceinline__ void stg_partial(uint16_t *p, const uint4 v, const int nv) {
+    const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        if (c < nv) p[c] = (uint16_t)(q[c >> 1] >> (16 * (c & 1)));
+}
+
+// zero the pixels at and beyond column nv (0..8) of a lane
+__device__ __forceinline__ uint4 mask_cols(const uint4 v, const int nv) {
+    uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t keep = (2 * k < nv ? 0x0000FFFFu : 0u) | (2 * k + 1 < nv ? 0xFFFF0000u : 0u);
+        q[k] &= keep;
+    }
+    return make_uint4(q[0], q[1], q[2], q[3]);
+}
+
 __device__ __forceinline__ uint4 max3_u16x8(const uint4 a, const uint4 b, const uint4 c) {
     // __vmaxu2(__vmaxu2(.)) pairs fuse into one VIMNMX3.U16x2 each
     return make_uint4(__vmaxu2(__vmaxu2(a.x, b.x), c.x), __vmaxu2(__vmaxu2(a.y, b.y), c.y),
@@ -342,10 +424,12 @@ __device__ __forceinline__ uint32_t redux_add(uint32_t v) {
 
 // Row table entry of canvas row u for one slice (producer lanes).  Returns whether
 // the row is live (inside the window and the slice's span).
-template <int INTERP, int FORMULA>
+// Row-copy mode: frame row j of the slice sits at byte (d0 + 2*j*rs) & 15 of its slot (d0: the
+// alignment of row 0's first pixel of the tile); TMA mode: d0 = rs2 = 0.
+template <int INTERP, int FORMULA, int AC>
 __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int64_t lo, int64_t hi, double off,
                                          int64_t h, int64_t box_r0, int64_t box_rows, uint32_t box_addr,
-                                         uint32_t zero_addr) {
+                                         uint32_t zero_addr, uint32_t d0, uint32_t rs2) {
     o.c0 = 1.0;
     o.c1 = 0.0;
     o.n0 = -kTwo52;
@@ -362,8 +446,9 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     // the box covers [box_r0, box_r0 + TU + 2*slack): a tap outside it would read another
     // stage's data -- fail loudly instead (cheap: once per row per slice, producer warp only)
     if (rp.j0 < box_r0 || rp.j1 < box_r0 || rp.j0 - box_r0 >= box_rows || rp.j1 - box_r0 >= box_rows) __trap();
-    o.off_a = box_addr + (uint32_t)(rp.j0 - box_r0) * kRowBytes;
-    o.off_b = box_addr + (uint32_t)(rp.j1 - box_r0) * kRowBytes;
+    constexpr uint32_t pitch = 2u * row_pitch<AC>();
+    o.off_a = box_addr + (uint32_t)(rp.j0 - box_r0) * pitch + ((d0 + rs2 * (uint32_t)rp.j0) & 15u);
+    o.off_b = box_addr + (uint32_t)(rp.j1 - box_r0) * pitch + ((d0 + rs2 * (uint32_t)rp.j1) & 15u);
     if (rp.kind >= 2) {
         o.c0 = rp.c0;
         o.c1 = rp.c1;
@@ -383,10 +468,13 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
 // (the tap registers die before the accumulators are touched; XZ folds with 3-input maxes);
 // with 8 rows, and always in sum mode, each row is consumed as soon as it is computed (sums
 // take the u32 voxels straight from the rint, no pack/unpack: measured 2-5 % faster).
-template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN>
+// Row-copy mode (AC < 16), !FULL: a lane may straddle the right edge (nv < 8 pixels inside); its
+// outside pixels are zeroed before any reduction and never stored.
+template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN, int AC>
 __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off,
                                           uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
-                                          uint4 (&acc_max)[ROWS], uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
+                                          const int nv, uint4 (&acc_max)[ROWS],
+                                          uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
                                           uint4 &xz_max, uint32_t (&xz_sum)[8], uint32_t (&yzv)[ROWS]) {
     constexpr bool kStream = ROWS > 4 || !kMax;
     constexpr bool kFoldXz = kMax && SIDE && !kStream;  // XZ over the batch with 3-input maxes
@@ -394,8 +482,15 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     uint4 xz_prev = make_uint4(0, 0, 0, 0);
     const bool store = vrow != nullptr;
     constexpr bool chain = CHAIN && INTERP == SSB_INTERP_LINEAR;
-    auto consume = [&](const int k, const uint4 v) {
-        if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, v);
+    constexpr bool kEdge = AC != 16 && !FULL;  // a lane may straddle the right edge
+    auto put = [&](const int k, const uint4 v) {
+        if (!(store && (FULL || (k < rows_ok && col_ok)))) return;
+        if (kEdge && nv < 8) stg_partial(vrow + k * w, v, nv);
+        else stg8<AC>(vrow + k * w, v);
+    };
+    auto consume = [&](const int k, uint4 v) {
+        if (kEdge) v = mask_cols(v, nv);
+        put(k, v);
         if (kMax) {
             acc_max[k] = max_u16x8(acc_max[k], v);
             if (SIDE) {  // XZ / YZ requested (compile-time: XY-only views skip this work)
@@ -424,16 +519,16 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     };
     uint4 vs[kStream ? 1 : ROWS];
     double prev[8];
-    if (chain) to_biased8(lds128(rg[0].off_a + lane_off), prev);
+    if (chain) to_biased8(lds8<AC>(rg[0].off_a + lane_off), prev);
 #pragma unroll
     for (int k = 0; k < ROWS; ++k) {
         uint4 v;
         if (INTERP == SSB_INTERP_NEAREST) {
-            v = lds128(rg[k].off_a + lane_off);
+            v = lds8<AC>(rg[k].off_a + lane_off);
         } else if (chain) {
             // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
             double cur[8];
-            to_biased8(lds128(rg[k].off_b + lane_off), cur);
+            to_biased8(lds8<AC>(rg[k].off_b + lane_off), cur);
             uint32_t r[8];
             if (FORMULA == SSB_FORMULA_NPINTERP) np_biased8_raw(prev, cur, rg[k].c0, r);
             else lerp_biased8_raw(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1, r);
@@ -441,7 +536,11 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                 // sums take the rounded voxels straight from the rint trick (no unpacking)
 #pragma unroll
                 for (int c = 0; c < 8; ++c) prev[c] = cur[c];
-                if (store && (FULL || (k < rows_ok && col_ok))) stg_cs_v4(vrow + k * w, pack8(r));
+                if (kEdge) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) r[c] = c < nv ? r[c] : 0u;
+                }
+                put(k, pack8(r));
                 uint32_t rs = 0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
@@ -458,10 +557,10 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
 #pragma unroll
             for (int c = 0; c < 8; ++c) prev[c] = cur[c];
         } else {
-            v = voxels8<FORMULA>(lds128(rg[k].off_a + lane_off), lds128(rg[k].off_b + lane_off), rg[k]);
+            v = voxels8<FORMULA>(lds8<AC>(rg[k].off_a + lane_off), lds8<AC>(rg[k].off_b + lane_off), rg[k]);
         }
         if (kStream) consume(k, v);
-        else vs[k] = v;
+        else vs[k] = kEdge ? mask_cols(v, nv) : v;
     }
     if (!kStream) {
         if (kFoldXz) {
@@ -473,7 +572,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     }
 }
 
-template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE>
+template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
 __global__ void __launch_bounds__(kThreads, 1)
     deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
@@ -482,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kStages = C::kStages;
     constexpr int kXzBatch = kMax ? C::kXzBatch : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem<ROWS> &sm = *reinterpret_cast<Smem<ROWS> *>(smem_raw);
+    Smem<ROWS, AC> &sm = *reinterpret_cast<Smem<ROWS, AC> *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
@@ -496,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_mbar_init();
     }
-    for (int k = tid; k < kTX; k += kThreads) sm.zero_row[k] = 0;
+    for (int k = tid; k < kTX + 8; k += kThreads) sm.zero_row[k] = 0;
     __syncthreads();
 
     if (warp == kConsumerWarps) {
@@ -530,15 +629,58 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t box_r0 = tu0 - base - box_slack<INTERP, FORMULA>();
                 // the box load goes out as soon as the stage is free; the row table is built
                 // while it is in flight (full completes on the bytes + all 32 lane arrivals)
+                constexpr int kBoxRowsUsed = C::template box_rows<INTERP, FORMULA>();
                 if (lane == 0) {
                     mbar_wait(&sm.empty[stage], sphase ^ 1);
-                    if (hit) {
-                        mbar_expect_tx(&sm.full[stage], C::template box_rows<INTERP, FORMULA>() * kRowBytes);
+                    if (hit && AC == 16) {
+                        mbar_expect_tx(&sm.full[stage], kBoxRowsUsed * kRowBytes);
                         tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
                                     (int32_t)s, policy);
                     }
                 }
                 __syncwarp();
+                // row-copy mode: tile row 0's first pixel, and per frame row the byte step
+                uint32_t d0 = 0, rs2 = 0;
+                if (AC != 16) {
+                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p.raw) +
+                                         2u * (uintptr_t)(s * p.frame_stride + (int64_t)xt * kTX);
+                    d0 = (uint32_t)(a0 & 15u);
+                    rs2 = (uint32_t)((2 * p.row_stride) & 15);
+                    if (hit) {
+                        // one bulk copy per frame row inside [0, H): the row's 16-byte-aligned superset
+                        const int64_t ncols = min((int64_t)kTX, p.w - (int64_t)xt * kTX);
+                        uint32_t bytes[(kBoxRowsUsed + 31) / 32];
+                        uint64_t src[(kBoxRowsUsed + 31) / 32];
+                        uint32_t total = 0;
+#pragma unroll
+                        for (int j = 0; j < (kBoxRowsUsed + 31) / 32; ++j) {
+                            const int r = lane + 32 * j;
+                            const int64_t jr = box_r0 + r;
+                            bytes[j] = 0;
+                            src[j] = 0;
+                            if (r < kBoxRowsUsed && jr >= 0 && jr < p.h) {
+                                const uintptr_t a = a0 + 2u * (uintptr_t)(jr * p.row_stride);
+                                const uint32_t lead = (uint32_t)(a & 15u);
+                                src[j] = (uint64_t)(a - lead);
+                                bytes[j] = (lead + 2u * (uint32_t)ncols + 15u) & ~15u;
+                                total += bytes[j];
+                            }
+                        }
+                        total = redux_add(total);
+                        if (lane == 0) mbar_expect_tx(&sm.full[stage], total);
+                        __syncwarp();
+#pragma unroll
+                        for (int j = 0; j < (kBoxRowsUsed + 31) / 32; ++j) {
+                            if (bytes[j] == 0) continue;
+                            const int r = lane + 32 * j;
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                                " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(&sm.box[stage][r][0])),
+                                "l"(src[j]), "r"(bytes[j]), "r"(smem_addr(&sm.full[stage])), "l"(policy)
+                                : "memory");
+                        }
+                    }
+                }
                 uint32_t live[C::kRowWords];
 #pragma unroll
                 for (int j = 0; j < C::kRowWords; ++j) live[j] = 0;
@@ -549,10 +691,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int r = lane + 32 * j;
                         bool l = false;
                         if (r < kTU)
-                            l = make_row<INTERP, FORMULA>(sm.rows[stage][r], tu0 + r,
-                                                          (int64_t)ut * kTU + r < p.u_count, lo, hi, off, p.h,
-                                                          box_r0, C::template box_rows<INTERP, FORMULA>(), box_addr,
-                                                          zero_addr);
+                            l = make_row<INTERP, FORMULA, AC>(sm.rows[stage][r], tu0 + r,
+                                                              (int64_t)ut * kTU + r < p.u_count, lo, hi, off, p.h,
+                                                              box_r0, C::template box_rows<INTERP, FORMULA>(),
+                                                              box_addr, zero_addr, d0, rs2);
                         live[j] = __ballot_sync(0xffffffffu, l);
                     }
                 }
@@ -608,12 +750,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode<kTU>(item, p, ut, xt, s_begin, s_end);
         const int64_t x = (int64_t)xt * kTX + lane * 8;
         const bool col_ok = x < p.w;
+        const int nv = (int)max((int64_t)0, min((int64_t)8, p.w - x));  // this lane's pixels inside
         const int64_t r0 = (int64_t)ut * kTU + warp * ROWS;  // window row of k = 0
         const int64_t rows_left = p.u_count - r0;
         const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= ROWS ? ROWS : (int)rows_left);
         uint16_t *vrow = p.vol != nullptr ? p.vol + (size_t)s_begin * plane + (size_t)r0 * p.w + x : nullptr;
         // warp-uniform fast path: every lane's 8 columns and all rows inside the output
-        const bool fast = __all_sync(0xffffffffu, col_ok) && rows_ok == ROWS;
+        const bool fast = __all_sync(0xffffffffu, AC == 16 ? col_ok : nv == 8) && rows_ok == ROWS;
         uint32_t *yzp = p.yz != nullptr ? p.yz + (size_t)s_begin * p.u_count + r0 + lane : nullptr;
         const bool has_xz = p.xz != nullptr;
         int g = 0;  // slice within the current XZ batch
@@ -644,28 +787,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // four specialisations so the row loop has no per-row branches
                 if (fast) {
                     if (chained)
-                        rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE, true>(rg, lane_off, vrow, p.w, rows_ok,
-                                                                                col_ok, acc_max, acc_sum, xz_max,
+                        rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE, true, AC>(rg, lane_off, vrow, p.w, rows_ok,
+                                                                                col_ok, nv, acc_max, acc_sum, xz_max,
                                                                                 xz_sum, yzv);
                     else
-                        rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE, false>(rg, lane_off, vrow, p.w, rows_ok,
-                                                                                 col_ok, acc_max, acc_sum, xz_max,
+                        rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE, false, AC>(rg, lane_off, vrow, p.w, rows_ok,
+                                                                                 col_ok, nv, acc_max, acc_sum, xz_max,
                                                                                  xz_sum, yzv);
                 } else {
                     if (chained)
-                        rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE, true>(rg, lane_off, vrow, p.w, rows_ok,
-                                                                                 col_ok, acc_max, acc_sum, xz_max,
+                        rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE, true, AC>(rg, lane_off, vrow, p.w, rows_ok,
+                                                                                 col_ok, nv, acc_max, acc_sum, xz_max,
                                                                                  xz_sum, yzv);
                     else
-                        rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE, false>(rg, lane_off, vrow, p.w, rows_ok,
-                                                                                  col_ok, acc_max, acc_sum, xz_max,
+                        rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE, false, AC>(rg, lane_off, vrow, p.w, rows_ok,
+                                                                                  col_ok, nv, acc_max, acc_sum, xz_max,
                                                                                   xz_sum, yzv);
                 }
             } else if (vrow != nullptr && col_ok) {
                 const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
-                for (int k = 0; k < ROWS; ++k)
-                    if (k < rows_ok) stg_cs_v4(vrow + (size_t)k * p.w, z);
+                for (int k = 0; k < ROWS; ++k) {
+                    if (k >= rows_ok) continue;
+                    if (AC != 16 && nv < 8) stg_partial(vrow + (size_t)k * p.w, z, nv);
+                    else stg8<AC>(vrow + (size_t)k * p.w, z);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.empty[stage]);
@@ -737,12 +883,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
                         const uint32_t e = (w4[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
-                        if (e) red_u32<true>(dst + c, e);
+                        if (e && (AC == 16 || c < nv)) red_u32<true>(dst + c, e);
                     }
                 } else {
 #pragma unroll
                     for (int c = 0; c < 8; ++c)
-                        if (acc_sum[k][c]) red_u32<false>(dst + c, acc_sum[k][c]);
+                        if (acc_sum[k][c] && (AC == 16 || c < nv)) red_u32<false>(dst + c, acc_sum[k][c]);
                 }
             }
         }
@@ -804,28 +950,42 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE = true>
+template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
 int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
-    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE>;
-    constexpr int smem = (int)sizeof(Smem<ROWS>);
+    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC>;
+    constexpr int smem = (int)sizeof(Smem<ROWS, AC>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<grid, kThreads, smem, st>>>(map, prm);
     return check_launch("deskew_tma_kernel");
 }
 
 // Kernel instantiation for (reduce, tile height, side projections requested):
-//   max: 4 rows {with, without XZ/YZ}, 8 rows with XZ/YZ (projection-only)    sum: 4 rows {with, without}
-template <int INTERP, int FORMULA>
+//   max: 4 rows {with, without XZ/YZ}, 8 rows with XZ/YZ (projection-only, TMA mode only)
+//   sum: 4 rows {with, without}
+template <int INTERP, int FORMULA, int AC>
 int launch_variant(bool mx, bool tall, bool side, const CUtensorMap &map, const Params &prm, int grid,
                    cudaStream_t st) {
     if (mx) {
-        if (side)
-            return tall ? launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 8, true>(map, prm, grid, st)
-                        : launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, true>(map, prm, grid, st);
-        return launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, false>(map, prm, grid, st);
+        if (side) {
+            if (AC == 16 && tall) return launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 8, true, 16>(map, prm, grid, st);
+            return launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, true, AC>(map, prm, grid, st);
+        }
+        return launch_one<INTERP, FORMULA, SSB_REDUCE_MAX, 4, false, AC>(map, prm, grid, st);
     }
-    if (side) return launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, true>(map, prm, grid, st);
-    return launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, false>(map, prm, grid, st);
+    if (side) return launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, true, AC>(map, prm, grid, st);
+    return launch_one<INTERP, FORMULA, SSB_REDUCE_SUM, 4, false, AC>(map, prm, grid, st);
+}
+
+template <int INTERP, int FORMULA>
+int launch_ac(int ac, bool mx, bool tall, bool side, const CUtensorMap &map, const Params &prm, int grid,
+              cudaStream_t st) {
+    if (ac == 16) return launch_variant<INTERP, FORMULA, 16>(mx, tall, side, map, prm, grid, st);
+    if constexpr (FORMULA == SSB_FORMULA_CANVAS) {  // row-copy mode: canvas formula (ProjectionCanvas) only
+        if (ac == 8) return launch_variant<INTERP, FORMULA, 8>(mx, false, side, map, prm, grid, st);
+        if (ac == 4) return launch_variant<INTERP, FORMULA, 4>(mx, false, side, map, prm, grid, st);
+        if (ac == 2) return launch_variant<INTERP, FORMULA, 2>(mx, false, side, map, prm, grid, st);
+    }
+    return fail(SSB_ERR_PARAM, "no persistent kernel for access class %d", ac);
 }
 
 }  // namespace tma_path
@@ -835,6 +995,23 @@ bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol
     if (row_stride_of(d) % 8 != 0 || frame_stride_of(d) % 8 != 0) return false;  // TMA: 16-byte strides
     if (d.n > INT32_MAX || d.height > INT32_MAX || d.width > INT32_MAX) return false;
     return tma_path::encode_fn() != nullptr;
+}
+
+int persistent_access_class(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol, const void *xy) {
+    if (tma_eligible(d, raw, vol, xy)) return 16;
+    if (d.formula != SSB_FORMULA_CANVAS || getenv("SSB_DISABLE_ROWCOPY") != nullptr) return 0;
+    if (d.n > INT32_MAX || d.height > INT32_MAX || d.width > INT32_MAX) return 0;
+    if ((reinterpret_cast<uintptr_t>(xy) & 3u) != 0) return 0;  // u16 XY is written by the finalize pass
+    // widest access every frame row (loads from the row slots) and every volume row (stores) allows
+    const uintptr_t r = reinterpret_cast<uintptr_t>(raw), v = reinterpret_cast<uintptr_t>(vol);
+    const int64_t rs = row_stride_of(d), fs = frame_stride_of(d), w = d.width;
+    auto fits = [&](int ac) {
+        const int64_t e = ac / 2;
+        return (r % ac) == 0 && rs % e == 0 && fs % e == 0 && (vol == nullptr || ((v % ac) == 0 && w % e == 0));
+    };
+    const int ac = fits(8) ? 8 : fits(4) ? 4 : 2;
+    const char *force = getenv("SSB_FORCE_AC");  // A/B and debugging: a narrower class than allowed
+    return force && atoi(force) < ac && (atoi(force) == 4 || atoi(force) == 2) ? atoi(force) : ac;
 }
 
 namespace {
@@ -856,12 +1033,13 @@ size_t tma_workspace_bytes(const ssb_deskew_desc &d) {
 }
 
 int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz, void *yz,
-                      void *workspace, size_t workspace_bytes, cudaStream_t st) {
+                      void *workspace, size_t workspace_bytes, cudaStream_t st, int ac) {
     using namespace tma_path;
     if (workspace == nullptr || workspace_bytes < tma_workspace_bytes(d))
         return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", tma_workspace_bytes(d),
                     workspace_bytes);
     CUtensorMap map;
+    memset(&map, 0, sizeof map);
     const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)d.n};
     const cuuint64_t strides[2] = {(cuuint64_t)row_stride_of(d) * 2, (cuuint64_t)frame_stride_of(d) * 2};
     const bool mx = d.reduce == SSB_REDUCE_MAX;
@@ -869,7 +1047,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     // 8-row tiles pay only where the per-row XZ/YZ work dominates: projection-only max with side
     // projections (measured: XY-only is faster with 4-row tiles and their deeper 5-stage ring)
     const int64_t tall_env = env_i64("SSB_TALL_TILES", 1);  // 0 never, 1 projection-only, 2 always (A/B)
-    const bool tall = (vol == nullptr || tall_env == 2) && tall_env != 0 && mx && side;
+    const bool tall = (vol == nullptr || tall_env == 2) && tall_env != 0 && mx && side && ac == 16;
     const int kTU = tall ? Cfg<8>::kTU : Cfg<4>::kTU;
     const int slack = d.interp == SSB_INTERP_NEAREST ? box_slack<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
                       : d.formula == SSB_FORMULA_CANVAS ? box_slack<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>()
@@ -877,10 +1055,12 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     const int rows = kTU + 2 * slack;
     const cuuint32_t box[3] = {(cuuint32_t)kTX, (cuuint32_t)rows, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t *>(raw), dims,
-                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SSB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    if (ac == 16) {  // row-copy mode (ac < 16) addresses the frames directly
+        const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t *>(raw), dims,
+                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(SSB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
 
     // work items: (u-tile, x-tile, slice chunk); ~kItemsPerCta items per persistent CTA keep the
     // dynamic scheduler's tail short (projections reduce in L2, so chunking costs no partial planes)
@@ -972,17 +1152,20 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     prm.xy_accumulate = acc;
     prm.clip = clip ? 1 : 0;
     prm.big_pct = (int32_t)big_pct;
+    prm.raw = raw;
+    prm.row_stride = row_stride_of(d);
+    prm.frame_stride = frame_stride_of(d);
     const int grid = (int)std::min<int64_t>(items, sms);
 
     int rc;
     profile_begin(st);
     // one place decides the instantiation, consistent with the tile height planned above
     if (d.interp == SSB_INTERP_NEAREST)
-        rc = launch_variant<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>(mx, tall, side, map, prm, grid, st);
+        rc = launch_ac<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>(ac, mx, tall, side, map, prm, grid, st);
     else if (d.formula == SSB_FORMULA_CANVAS)
-        rc = launch_variant<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>(mx, tall, side, map, prm, grid, st);
+        rc = launch_ac<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>(ac, mx, tall, side, map, prm, grid, st);
     else
-        rc = launch_variant<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>(mx, tall, side, map, prm, grid, st);
+        rc = launch_ac<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>(ac, mx, tall, side, map, prm, grid, st);
     profile_end(st);
     count_launches(1);
     if (rc) return rc;

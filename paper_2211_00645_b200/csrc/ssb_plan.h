@@ -22,8 +22,13 @@ bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol
 // Workspace the TMA path needs (scheduler counter + u32 reduction scratch for max mode).
 size_t tma_workspace_bytes(const ssb_deskew_desc &d);
 
-// Launch the persistent TMA kernel (+ scratch resets and the u32 -> u16 finalize).
+// Access class of the persistent kernel for this call: 16 = TMA boxes (16-byte aligned rows);
+// 8 / 4 / 2 = row-copy mode (1-D bulk copies per frame row, AC-byte shared loads and volume
+// stores); 0 = use the generic tiled kernel.
+int persistent_access_class(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol, const void *xy);
+
+// Launch the persistent kernel (+ scratch resets and the u32 -> u16 finalize).
 int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz, void *yz,
-                      void *workspace, size_t workspace_bytes, cudaStream_t st);
+                      void *workspace, size_t workspace_bytes, cudaStream_t st, int ac);
 
 }  // namespace ssb
