@@ -104,13 +104,22 @@ struct Params {
 };
 
 // AC: 16 = rows reach shared memory through one 3-D TMA box (16-byte aligned rows);
-// 8 / 4 / 2 = row-copy mode for rows that are not 16-byte aligned (W % 8 != 0, offset crops): the
-// producer issues one 1-D bulk copy per frame row of the row's 16-byte-aligned superset into a
-// 528-byte slot, the row table points each tap at its first pixel inside the slot, and consumers
-// read / write 8 pixels with accesses of AC bytes (the widest every row's alignment allows).
+// 8 = rows 8-byte aligned (e.g. W % 8 == 4): the producer lanes copy each row's 256 pixels with
+// 8-byte cp.async into the same 16-byte aligned layout as the TMA box;
+// 4 / 2 = rows 4- / 2-byte aligned: one 1-D bulk copy per frame row of its 16-byte-aligned
+// superset into a 528-byte slot, the row table points each tap at its first pixel inside the slot
+// and consumers read with 4- / 2-byte granularity.  Volume stores use AC-byte accesses.
+// Measured at 512 x 2048 x W (B200): W = 2044 (AC 8) 2.84 ms, 2046 (AC 4) 3.13 ms, 2047 (AC 2)
+// 3.65 ms, against 1.65 ms for TMA boxes at W = 2048 -- the producer's per-row copy issue, not
+// HBM, bounds these modes.
 template <int AC>
 __host__ __device__ constexpr int row_pitch() {
-    return AC == 16 ? kTX : kTX + 8;
+    return AC <= 4 ? kTX + 8 : kTX;
+}
+// shared-memory rows are 16-byte aligned except in bulk-copy mode (AC <= 4)
+template <int AC>
+__host__ __device__ constexpr int smem_ac() {
+    return AC <= 4 ? AC : 16;
 }
 
 template <int ROWS, int AC = 16>
@@ -519,16 +528,16 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     };
     uint4 vs[kStream ? 1 : ROWS];
     double prev[8];
-    if (chain) to_biased8(lds8<AC>(rg[0].off_a + lane_off), prev);
+    if (chain) to_biased8(lds8<smem_ac<AC>()>(rg[0].off_a + lane_off), prev);
 #pragma unroll
     for (int k = 0; k < ROWS; ++k) {
         uint4 v;
         if (INTERP == SSB_INTERP_NEAREST) {
-            v = lds8<AC>(rg[k].off_a + lane_off);
+            v = lds8<smem_ac<AC>()>(rg[k].off_a + lane_off);
         } else if (chain) {
             // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
             double cur[8];
-            to_biased8(lds8<AC>(rg[k].off_b + lane_off), cur);
+            to_biased8(lds8<smem_ac<AC>()>(rg[k].off_b + lane_off), cur);
             uint32_t r[8];
             if (FORMULA == SSB_FORMULA_NPINTERP) np_biased8_raw(prev, cur, rg[k].c0, r);
             else lerp_biased8_raw(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1, r);
@@ -557,7 +566,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
 #pragma unroll
             for (int c = 0; c < 8; ++c) prev[c] = cur[c];
         } else {
-            v = voxels8<FORMULA>(lds8<AC>(rg[k].off_a + lane_off), lds8<AC>(rg[k].off_b + lane_off), rg[k]);
+            v = voxels8<FORMULA>(lds8<smem_ac<AC>()>(rg[k].off_a + lane_off), lds8<smem_ac<AC>()>(rg[k].off_b + lane_off), rg[k]);
         }
         if (kStream) consume(k, v);
         else vs[k] = kEdge ? mask_cols(v, nv) : v;
@@ -586,7 +595,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (tid == 0) {
         for (int k = 0; k < kStages; ++k) {
-            mbar_init(&sm.full[k], 32);
+            // cp.async modes add one asynchronous arrival per producer lane (copies landed)
+            mbar_init(&sm.full[k], AC == 8 ? 64 : 32);
             mbar_init(&sm.empty[k], kConsumerWarps);
         }
         for (int k = 0; k < kQueue; ++k) {
@@ -641,7 +651,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 // row-copy mode: tile row 0's first pixel, and per frame row the byte step
                 uint32_t d0 = 0, rs2 = 0;
-                if (AC != 16) {
+                if (AC == 8) {
+                    if (hit) {
+                        // each lane copies its 8 pixels of every frame row inside [0, H) in AC-byte
+                        // pieces (pieces starting at or past the row end are skipped)
+                        const int64_t x0 = (int64_t)xt * kTX + lane * 8;
+                        const int npix = (int)max((int64_t)0, min((int64_t)8, p.w - x0));
+                        const int r_lo = (int)max((int64_t)0, -box_r0);
+                        const int r_hi = (int)min((int64_t)kBoxRowsUsed, p.h - box_r0);
+                        const char *src = reinterpret_cast<const char *>(p.raw) +
+                                          2 * (s * p.frame_stride + (box_r0 + r_lo) * p.row_stride + x0);
+                        const int64_t step = 2 * p.row_stride;
+                        uint32_t dst = smem_addr(&sm.box[stage][r_lo][0]) + 16u * lane;
+                        constexpr int kPix = AC / 2;
+                        for (int r = r_lo; r < r_hi; ++r, src += step, dst += 2u * kTX) {
+#pragma unroll
+                            for (int q = 0; q < 8 / kPix; ++q) {
+                                if (q * kPix < npix)
+                                    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst + q * AC),
+                                                 "l"(src + q * AC), "n"(AC)
+                                                 : "memory");
+                            }
+                        }
+                    }
+                    // arrives (no increment) on `full` once this lane's copies have landed
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&sm.full[stage]))
+                                 : "memory");
+                }
+                if (AC <= 4) {
                     const uintptr_t a0 = reinterpret_cast<uintptr_t>(p.raw) +
                                          2u * (uintptr_t)(s * p.frame_stride + (int64_t)xt * kTX);
                     d0 = (uint32_t)(a0 & 15u);
