@@ -19,7 +19,10 @@
 //    XY (registers), YZ (REDUX) and XZ (shared memory, named barrier) reductions, which
 //    land in u32 scratch through L2 reductions (red.global.max/add);
 //  * int->double conversion is folded into the products: fma(w, 2^52 + a,
-//    -w*2^52) == fl(w*a) exactly (one rounding), so a voxel costs 2 DFMA + 2 DADD.
+//    -w*2^52) == fl(w*a) exactly (one rounding), so a voxel costs 2 DFMA + 2 DADD;
+//  * rows that are not 16-byte aligned (W % 8 != 0, odd-offset crops) run the same pipeline
+//    in row-copy mode (template AC < 16): cp.async or per-row 1-D bulk copies instead of the
+//    TMA box, narrower shared loads / volume stores, right-edge lanes masked (see Smem).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
