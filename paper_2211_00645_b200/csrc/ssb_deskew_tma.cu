@@ -1132,7 +1132,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     if (n1 < 1) n1 = n_plan;
     int64_t S, chunk, S2, chunk2;
     split(n1, per1, S, chunk);
-    split(n_plan - n1, env_i64("SSB_TAIL_ITEMS_PER_CTA", 6), S2, chunk2);
+    split(n_plan - n1, env_i64("SSB_TAIL_ITEMS_PER_CTA", 3), S2, chunk2);
     const int64_t items = tiles * (S + S2);
     if (items > INT32_MAX / 2) return fail(SSB_ERR_CAPACITY, "too many tiles");
 
