@@ -137,10 +137,10 @@ class ChannelDeskewer:
         else:
             # page-locked landing buffer (cached by torch's host allocator), owned by the image
             host = torch.empty(tuple(image.shape), dtype=torch.int16, pin_memory=True)
-            host.copy_(image.view(torch.int16), non_blocking=True)
-            torch.cuda.current_stream(image.device).wait_stream(self.stream)
-            host_done = torch.cuda.Event()
-            host_done.record(self.stream)
+            with torch.cuda.stream(self.stream):  # the copy and the event on the canvas stream
+                host.copy_(image.view(torch.int16), non_blocking=True)
+                host_done = torch.cuda.Event()
+                host_done.record(self.stream)
             host_done.synchronize()
             pixels = host.numpy().view(np.uint16)
         t1 = self.clock_ns()
