@@ -33,7 +33,13 @@ from .geometry import row_span, _ceil_snapped
 
 @dataclass(frozen=True)
 class SlabPlan:
-    """One rank's share of a long scan."""
+    """One rank's share of a long scan.
+
+    The rank owns output slices [first, first + count).  Its INPUT may extend by halo planes
+    on either side (clipped at the scan ends): frames [in_first, in_first + in_count).  Both
+    reference interpolations read only a slice's own frame (ss/pipeline.py:283-290), so the
+    default halo is 0; a cross-frame interpolation would read its neighbours from the halo.
+    """
 
     rank: int
     first: int        # global index of the slab's first frame
@@ -41,14 +47,27 @@ class SlabPlan:
     u_begin: int      # first canvas row the slab touches
     u_count: int      # canvas rows it touches
     canvas_rows: int  # U of the whole scan
+    halo_lo: int = 0  # halo planes before `first` in the rank's input
+    halo_hi: int = 0  # halo planes after the slab
+
+    @property
+    def in_first(self) -> int:
+        return self.first - self.halo_lo
+
+    @property
+    def in_count(self) -> int:
+        return self.halo_lo + self.count + self.halo_hi
 
 
 def canvas_rows_total(n_total: int, height: int, shear_px: float) -> int:
     return height + _ceil_snapped((n_total - 1) * shear_px)  # ss/geometry.py:141
 
 
-def plan_slabs(n_total: int, height: int, shear_px: float, interp: str, world: int) -> list:
-    """Contiguous, near-equal slabs; canvas window = [lo(first), hi(last)] (spans are monotone in i)."""
+def plan_slabs(n_total: int, height: int, shear_px: float, interp: str, world: int, halo: int = 0) -> list:
+    """Contiguous, near-equal slabs; canvas window = [lo(first), hi(last)] (spans are monotone in i);
+    ``halo`` input planes on each side of a slab (clipped at the scan ends)."""
+    if halo < 0:
+        raise ValueError(f"halo must be >= 0, got {halo}")
     U = canvas_rows_total(n_total, height, shear_px)
     base, extra = divmod(n_total, world)
     plans, first = [], 0
@@ -60,7 +79,8 @@ def plan_slabs(n_total: int, height: int, shear_px: float, interp: str, world: i
         lo, _ = row_span(first, shear_px, height, interp)
         _, hi = row_span(first + count - 1, shear_px, height, interp)
         lo, hi = max(lo, 0), min(hi, U - 1)
-        plans.append(SlabPlan(r, first, count, lo, hi - lo + 1, U))
+        plans.append(SlabPlan(r, first, count, lo, hi - lo + 1, U, min(halo, first),
+                              min(halo, n_total - first - count)))
         first += count
     return plans
 
@@ -72,11 +92,17 @@ def shard_stacks(n_stacks: int, rank: int, world: int) -> list:
 
 def deskew_slab(raw_slab: torch.Tensor, plan: SlabPlan, shear_px: float, interp: str = "linear", *,
                 reduce: str = "sum", projection_axes=(0,), write_volume: bool = False, stream=None):
-    """Deskew this rank's frames over its canvas row window (device, one fused launch)."""
+    """Deskew this rank's frames over its canvas row window (device, one fused launch).
+
+    ``raw_slab`` holds the rank's input frames: the slab itself, or slab + halo planes
+    (``plan.in_count`` frames starting at global frame ``plan.in_first``)."""
     from .deskew import deskew_device
 
-    if int(raw_slab.shape[0]) != plan.count:
-        raise ValueError(f"slab holds {raw_slab.shape[0]} frames, plan says {plan.count}")
+    n_in = int(raw_slab.shape[0])
+    if n_in == plan.in_count and (plan.halo_lo or plan.halo_hi):
+        raw_slab = raw_slab[plan.halo_lo:plan.halo_lo + plan.count]  # the owned slices (a view)
+    elif n_in != plan.count:
+        raise ValueError(f"slab holds {n_in} frames, plan says {plan.count} (+ halo {plan.halo_lo}/{plan.halo_hi})")
     return deskew_device(raw_slab, shear_px, interp, first_slice=plan.first, canvas_rows=plan.canvas_rows,
                          u_begin=plan.u_begin, u_count=plan.u_count, projection_axes=projection_axes,
                          reduce=reduce, write_volume=write_volume, stream=stream)

@@ -121,3 +121,17 @@ def test_sum_combine_wraps_like_uint32(tmp_path):
     assert got.dtype == np.uint32
     np.testing.assert_array_equal(got, (want % (1 << 32)).astype(np.uint32))
     assert (want >= (1 << 32)).any()  # the case really wraps
+
+
+def test_halo_planes_in_the_plan():
+    """Slabs may carry halo input planes (north_star: scan-axis slabs with halo planes); they are
+    clipped at the scan ends and never change which slices a rank owns."""
+    plans = D.plan_slabs(100, 16, 0.7, "linear", 4, halo=3)
+    assert [p.count for p in plans] == [25] * 4
+    assert [(p.halo_lo, p.halo_hi) for p in plans] == [(0, 3), (3, 3), (3, 3), (3, 0)]
+    assert [(p.in_first, p.in_count) for p in plans] == [(0, 28), (22, 31), (47, 31), (72, 28)]
+    base = D.plan_slabs(100, 16, 0.7, "linear", 4)
+    assert [(p.first, p.count, p.u_begin, p.u_count) for p in plans] == \
+           [(p.first, p.count, p.u_begin, p.u_count) for p in base]
+    with pytest.raises(ValueError):
+        D.plan_slabs(10, 4, 1.0, "linear", 2, halo=-1)

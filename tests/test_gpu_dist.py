@@ -13,19 +13,19 @@ from paper_2211_00645_b200.deskew import deskew_device
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("world,halo", [(2, 0), (3, 0), (8, 0), (3, 2)])
 @pytest.mark.parametrize("reduce", ["sum", "max"])
-def test_slabs_merge_to_full_scan(world, reduce):
+def test_slabs_merge_to_full_scan(world, halo, reduce):
     n, h, w, s = 300, 96, 512, 0.7071067811865476
     g = torch.Generator(device="cuda").manual_seed(world)
     raw = torch.randint(0, 65536, (n, h, w), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
     full = deskew_device(raw, s, "linear", reduce=reduce, write_volume=False)
-    plans = D.plan_slabs(n, h, s, "linear", world)
+    plans = D.plan_slabs(n, h, s, "linear", world, halo=halo)
     U = plans[0].canvas_rows
     xy = torch.zeros((U, w), dtype=torch.int64, device="cuda")
     xz, yz = [], []
     for p in plans:
-        part = D.deskew_slab(raw[p.first:p.first + p.count], p, s, "linear", reduce=reduce,
+        part = D.deskew_slab(raw[p.in_first:p.in_first + p.in_count], p, s, "linear", reduce=reduce,
                              projection_axes=(0, 1, 2))
         win = part.projections[0].to(torch.int64)
         if reduce == "max":
