@@ -141,6 +141,9 @@ class ProjectionCanvas:
         self._roll_ws = None       # device list of voxels to re-max (incremental rolling updates)
         self._host_cache = None
         self._pending_uploads: list = []  # (copy-done event, pinned host buffer) still being read
+        self._staging = None              # pinned two-slot ring for pageable frames: (buffer, event)
+        self._stage_next = 0
+        self._stage_pending = None
         # True while canvas + contributor equal the full re-max over the ring, so a
         # rolling_replace can take the O(band) incremental path (see ssb_rolling_band)
         self._exact = True
@@ -160,23 +163,46 @@ class ProjectionCanvas:
         return all(rf is None for rf in self._ring)
 
     def _upload(self, pixels: np.ndarray) -> torch.Tensor:
-        """Frame -> device on the canvas stream; asynchronous when the frame already lives in
-        page-locked memory (e.g. a view of ``ingest.load_stack`` / ``stream.pinned_stack``)."""
+        """Frame -> device on the canvas stream, asynchronously.  Page-locked frames (e.g. views of
+        ``ingest.load_stack`` / ``stream.pinned_stack``) are copied directly; pageable frames are
+        first copied (multi-threaded) into a two-slot pinned staging ring, so the H2D copy of one
+        frame overlaps the host copy of the next instead of going through the driver's bounce
+        buffer synchronously."""
         host = torch.from_numpy(np.ascontiguousarray(pixels))
-        pinned = host.is_pinned()
+        if not host.is_pinned():
+            host = self._stage(host)
         with torch.cuda.stream(self.stream):
-            dev = host.to(self._device, non_blocking=pinned).unsqueeze(0)
-        if pinned:
-            # RawFrame pixels are immutable (ss/pipeline.py:37-39), so the copy may still be
-            # reading them after place() returns: hold the host buffer until its copy completes
-            self._hold_until_copied(host)
+            dev = host.to(self._device, non_blocking=True).unsqueeze(0)
+        # RawFrame pixels are immutable (ss/pipeline.py:37-39), so the copy may still be
+        # reading them after place() returns: hold the host buffer until its copy completes
+        self._hold_until_copied(host)
         return dev
+
+    def _stage(self, host: torch.Tensor) -> torch.Tensor:
+        """Copy a pageable frame into the next free slot of the pinned staging ring."""
+        ring = self._staging
+        if ring is None or tuple(ring[0][0].shape) != tuple(host.shape):
+            ring = self._staging = [(torch.empty(tuple(host.shape), dtype=host.dtype, pin_memory=True), None)
+                                    for _ in range(2)]
+        k = self._stage_next
+        self._stage_next ^= 1
+        buf, done = ring[k]
+        if done is not None:
+            done.synchronize()  # the H2D copy that last read this slot has finished
+        buf.copy_(host)
+        self._stage_pending = k  # _hold_until_copied attaches the slot's copy-done event
+        return buf
 
     def _hold_until_copied(self, host: torch.Tensor) -> None:
         """Keep a pinned host buffer alive until the asynchronous H2D copy just queued on the
         canvas stream has read it (the caller may drop the frame as soon as place() returns)."""
         done = torch.cuda.Event()
         done.record(self.stream)
+        if self._stage_pending is not None:  # a staging slot: free again once this copy is done
+            k = self._stage_pending
+            self._staging[k] = (self._staging[k][0], done)
+            self._stage_pending = None
+            return
         pending = [(e, h) for e, h in self._pending_uploads if not e.query()]
         pending.append((done, host))
         self._pending_uploads = pending
@@ -319,11 +345,11 @@ class ProjectionCanvas:
                 self._ring_dev = torch.zeros((n, h, w), dtype=torch.uint16, device=self._device)
                 self._present_dev = torch.zeros((n,), dtype=torch.uint8, device=self._device)
             host = torch.from_numpy(np.ascontiguousarray(frame.pixels))
-            pinned = host.is_pinned()
-            self._ring_dev[frame.slice_index].copy_(host, non_blocking=pinned)
+            if not host.is_pinned():
+                host = self._stage(host)  # pageable: through the pinned staging ring (see _upload)
+            self._ring_dev[frame.slice_index].copy_(host, non_blocking=True)
             self._present_dev[frame.slice_index] = 1
-        if pinned:
-            self._hold_until_copied(host)  # the async copy may still read it (see _upload)
+        self._hold_until_copied(host)  # the async copy may still read it
 
     def rolling_replace(self, frame: RawFrame) -> tuple[int, int]:
         """Swap in the newest version of a slice and refresh its band (ss/pipeline.py:345-359)."""
