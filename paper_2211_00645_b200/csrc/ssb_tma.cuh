@@ -63,13 +63,26 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 
 // Wait for an mbarrier phase.  A pipeline that can never complete (e.g. a transaction
-// count that does not match the TMA box) traps after ~4 s instead of hanging the GPU.
+// count that does not match the TMA box) traps instead of hanging the GPU.
+#ifndef SSB_WAIT_TIMER
+#define SSB_WAIT_TIMER 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
+#if SSB_WAIT_TIMER
     const uint64_t t0 = global_ns();
     while (!mbar_try_wait_sleep(bar, parity, 100000u)) {
         if (global_ns() - t0 > 4000000000ull) __trap();
     }
+#else
+    // every wake-up of a suspended warp costs issue slots, and waiting warps wake on unrelated
+    // barrier traffic several times per wait: count wake-ups instead of reading the global timer
+    // (each wake-up sleeps <= 100 us, so 2^24 of them bound the wait to minutes at worst)
+    uint32_t wakes = 0;
+    while (!mbar_try_wait_sleep(bar, parity, 100000u)) {
+        if (++wakes > (1u << 24)) __trap();
+    }
+#endif
 }
 
 // 3-D TMA tile load global -> shared, completion counted on an mbarrier.
