@@ -65,3 +65,18 @@ def test_native_restore_sphere(interp):
         sig_r = math.sqrt((f * (rows - r0) ** 2).sum() / tot)
         sig_c = math.sqrt((f * (cols - c0) ** 2).sum() / tot)
         assert abs(sig_r / sig_c - 1.0) <= 0.02
+
+
+def test_batch_views_match_reference_images():
+    """cli.run_batch's compute (one warped MIP per view angle, ss/cli.py:308-338) in one call,
+    against the reference's images for all four angles of the acceptance stack."""
+    from paper_2211_00645_b200.batch import deskew_views
+
+    st = A["a1_stack"]
+    g = g_of("a1_geom", st)
+    vts = [G.view_transform(g, view_angle_deg=float(t)) for t in A["a1_thetas"]]
+    images = deskew_views(st, g, vts, "linear")
+    for k, img in enumerate(images):
+        np.testing.assert_array_equal(img, A[f"a1_{k}_image"])
+    dev_imgs = deskew_views(torch.from_numpy(st).cuda(), g, vts[:1], "linear", device_outputs=True)
+    assert dev_imgs[0].is_cuda and np.array_equal(dev_imgs[0].cpu().numpy(), A["a1_0_image"])

@@ -104,6 +104,13 @@ class TestNoCpuFallback:
         with pytest.raises(ParameterError):
             deskew_device(torch.zeros((2, 4, 8), dtype=torch.uint16), 1.0)
 
+    def test_batch_views_need_device(self):
+        from paper_2211_00645_b200.batch import deskew_views
+        from paper_2211_00645_b200.geometry import view_transform
+        g = geom(n=2, w=8, h=4)
+        with pytest.raises(DeviceError):
+            deskew_views(np.zeros((2, 4, 8), np.uint16), g, [view_transform(g, view_angle_deg=30.0)])
+
     def test_warp_needs_device(self):
         with pytest.raises(DeviceError):
             pl.warp_projection(np.zeros((4, 2), np.uint16), 1.5)
