@@ -58,6 +58,9 @@ __host__ __device__ constexpr int box_slack() {
 // only max mode with XZ/YZ uses 8 rows (TU = 120, 3 stages), amortising the per-slice XZ
 // barrier and bookkeeping over twice the voxels.  Sum mode needs 8 u32 accumulators per row
 // and always keeps 4 rows.
+#ifndef SSB_YZ_LIVE_ONLY
+#define SSB_YZ_LIVE_ONLY 1  // A/B knob (profiles/README.md)
+#endif
 template <int ROWS>
 struct Cfg {
     static constexpr int kRows = ROWS;
@@ -797,8 +800,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint16_t *vrow = p.vol != nullptr ? p.vol + (size_t)s_begin * plane + (size_t)r0 * p.w + x : nullptr;
         // warp-uniform fast path: every lane's 8 columns and all rows inside the output
         const bool fast = __all_sync(0xffffffffu, AC == 16 ? col_ok : nv == 8) && rows_ok == ROWS;
-        uint32_t *yzp = p.yz != nullptr ? p.yz + (size_t)s_begin * p.u_count + r0 + lane : nullptr;
-        const bool has_xz = p.xz != nullptr;
+        // SIDE == false kernels run only without XZ / YZ outputs: their blocks compile away
+        uint32_t *yzp = (SIDE && p.yz != nullptr) ? p.yz + (size_t)s_begin * p.u_count + r0 + lane : nullptr;
+        const bool has_xz = SIDE && p.xz != nullptr;
         int g = 0;  // slice within the current XZ batch
 
         uint4 acc_max[ROWS];
@@ -859,6 +863,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (vrow != nullptr) vrow += plane;
 
             if (yzp != nullptr) {
+#if SSB_YZ_LIVE_ONLY
+                // dead passes have all-zero rows (neutral for max and sum): no RED, no lane select
+                if (live && lane < rows_ok) {
+                    uint32_t val = yzv[0];
+#pragma unroll
+                    for (int k = 1; k < ROWS; ++k)
+                        if (lane == k) val = yzv[k];
+                    red_u32<kMax>(yzp, val);
+                }
+#else
                 if (lane < rows_ok) {
                     uint32_t val = yzv[0];
 #pragma unroll
@@ -866,6 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (lane == k) val = yzv[k];
                     if (val != 0) red_u32<kMax>(yzp, val);
                 }
+#endif
                 yzp += p.u_count;
             }
 
