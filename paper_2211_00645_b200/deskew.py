@@ -93,20 +93,29 @@ def _vp(t):
 
 class _Workspaces:
     """One growable scratch buffer per CUDA stream (kernels on different streams
-    must not share partial-projection scratch)."""
+    must not share partial-projection scratch), least-recently-used streams evicted beyond
+    ``max_streams`` (callers that create streams per call, e.g. one StackStreamer per
+    ``deskew_volume``, would otherwise keep a buffer per pooled stream).  An evicted buffer is
+    released through torch's caching allocator, which orders its reuse after the work already
+    queued on its stream."""
 
-    def __init__(self):
+    def __init__(self, max_streams: int = 8):
+        from collections import OrderedDict
+
         self._lock = threading.Lock()
-        self._bufs: dict = {}
+        self._bufs = OrderedDict()
+        self.max_streams = max_streams
 
     def get(self, nbytes: int, stream: torch.cuda.Stream) -> torch.Tensor:
         key = (stream.device.index, stream.cuda_stream)
         with self._lock:
-            buf = self._bufs.get(key)
+            buf = self._bufs.pop(key, None)
             if buf is None or buf.numel() < nbytes:
                 with torch.cuda.stream(stream):
                     buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=stream.device)
-                self._bufs[key] = buf
+            self._bufs[key] = buf  # most recently used last
+            while len(self._bufs) > self.max_streams:
+                self._bufs.popitem(last=False)
             return buf
 
 
@@ -289,6 +298,9 @@ class DeskewGraph:
         self.result = deskew_device(raw, shear_px, interp, stream=self.stream, **kw)
         for _ in range(2):
             self._call()
+        # the graph bakes in this stream's scratch buffer: hold it, so an LRU eviction from the
+        # workspace cache cannot free memory the graph still writes
+        self._workspace = _workspaces.get(1, self.stream)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, stream=self.stream):
             self._call()

@@ -138,3 +138,26 @@ class TestChunkBounds:
         assert b[-1] == (192, 200) and len(b) == 7
         b = chunk_bounds(64, 32, 8)
         assert b == [(0, 32), (32, 56), (56, 64)]
+
+
+class TestWorkspaceCache:
+    def test_lru_bound(self):
+        """Scratch buffers are kept per stream, least recently used evicted (CPU stand-in streams)."""
+        from paper_2211_00645_b200.deskew import _Workspaces
+
+        class FakeStream:
+            def __init__(self, h):
+                self.cuda_stream = h
+                self.device = torch.device("cpu")
+
+        ws = _Workspaces(max_streams=3)
+        import contextlib
+        orig = torch.cuda.stream
+        torch.cuda.stream = lambda s: contextlib.nullcontext()
+        try:
+            bufs = [ws.get(1000, FakeStream(h)) for h in range(5)]
+            assert len(ws._bufs) == 3
+            assert ws.get(10, FakeStream(4)) is bufs[4]  # recent entry reused
+            assert ws.get(10, FakeStream(0)) is not bufs[0]  # evicted entry re-created
+        finally:
+            torch.cuda.stream = orig
