@@ -99,7 +99,7 @@ class _Workspaces:
     released through torch's caching allocator, which orders its reuse after the work already
     queued on its stream."""
 
-    def __init__(self, max_streams: int = 8):
+    def __init__(self, max_streams: int = 16):
         from collections import OrderedDict
 
         self._lock = threading.Lock()
