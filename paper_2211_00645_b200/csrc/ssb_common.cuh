@@ -15,6 +15,10 @@
 
 #include "ssb.h"
 
+#ifndef SSB_STORE_WB
+#define SSB_STORE_WB 0
+#endif
+
 namespace ssb {
 
 constexpr double kEps = 1e-9;                      // ss/geometry.py:39
@@ -159,6 +163,12 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void *p) {
 }
 
 __device__ __forceinline__ void stg_cs_v4(void *p, uint4 v) {
+#if SSB_STORE_WB  // A/B knob: default write-back stores instead of streaming (.cs)
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+    return;
+#endif
     asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
                  "r"(v.z), "r"(v.w)
                  : "memory");

@@ -58,6 +58,9 @@ __host__ __device__ constexpr int box_slack() {
 // only max mode with XZ/YZ uses 8 rows (TU = 120, 3 stages), amortising the per-slice XZ
 // barrier and bookkeeping over twice the voxels.  Sum mode needs 8 u32 accumulators per row
 // and always keeps 4 rows.
+#ifndef SSB_L2_PROMO  // A/B knob: L2 promotion of the TMA box loads
+#define SSB_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+#endif
 #ifndef SSB_YZ_LIVE_ONLY
 #define SSB_YZ_LIVE_ONLY 1  // A/B knob (profiles/README.md)
 #endif
@@ -1113,7 +1116,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     if (ac == 16) {  // row-copy mode (ac < 16) addresses the frames directly
         const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t *>(raw), dims,
                                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                       SSB_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SSB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
 
