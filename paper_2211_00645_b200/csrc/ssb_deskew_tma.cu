@@ -627,7 +627,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // halo rows shared by vertically adjacent tiles survive), evict-first in sum mode (whose u32
         // REDs into the caller's outputs want the L2 space; evict-normal was 2 % slower there)
         uint64_t policy;
-        if (kMax && SSB_LOAD_EVICT_NORMAL)
+        if (kMax && SSB_LOAD_EVICT_NORMAL == 2)
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
+        else if (kMax && SSB_LOAD_EVICT_NORMAL)
             asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
         else
             policy = policy_evict_first();
