@@ -133,16 +133,18 @@ def _cpu_worker(args):
     from oracle import deskew_oracle as O
 
     rng = np.random.default_rng(seed)
-    frames = rng.integers(0, 4096, size=(n_frames, h, w)).astype(np.uint16)
+    # a few distinct frames cycled (per-frame work does not depend on the values; generating
+    # every frame would dominate the wall time and hold GBs of host memory per worker)
+    frames = rng.integers(0, 4096, size=(min(n_frames, 4), h, w)).astype(np.uint16)
     canvas = np.zeros((u, w), dtype=np.uint16)
     t0 = time.perf_counter()
     for k in range(n_frames):
-        lo, hi, rows = O.slice_rows(frames[k], first + k, s, interp, "canvas")
+        lo, hi, rows = O.slice_rows(frames[k % len(frames)], first + k, s, interp, "canvas")
         np.maximum(canvas[lo:hi + 1], rows, out=canvas[lo:hi + 1])  # ss/pipeline.py:321
     return time.perf_counter() - t0
 
 
-def cpu_reference_sample(cfg, interp, target_s=12.0, cores=None):
+def cpu_reference_sample(cfg, interp, target_s=12.0, cores=None, pool=None):
     """Process-parallel reference port on a bounded sample; returns (GVox/s, detail)."""
     n, h, w = cfg["n"], cfg["h"], cfg["w"]
     s = native_shear(cfg["alpha"])
@@ -153,8 +155,11 @@ def cpu_reference_sample(cfg, interp, target_s=12.0, cores=None):
     per_worker = max(1, min(n, int(target_s / max(t1, 1e-4))))
     jobs = [(per_worker, (k * per_worker) % max(1, n - per_worker), h, w, s, u, interp, k + 1) for k in range(cores)]
     t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(cores) as pool:
+    if pool is not None:
         times = pool.map(_cpu_worker, jobs)
+    else:
+        with mp.get_context("fork").Pool(cores) as p:
+            times = p.map(_cpu_worker, jobs)
     wall = time.perf_counter() - t0
     frames = per_worker * cores
     busy = max(times)
@@ -173,12 +178,15 @@ def run_reference(args, cfg, rank, world):
         return
     interp = args.interp
     steps = []
-    for _ in range(max(1, args.warmup_ref)):
-        cpu_reference_sample(cfg, interp, target_s=2.0)
-    per_step = min(args.ref_seconds, max(1.0, 150.0 / max(1, args.steps)))
-    for _ in range(args.steps):
-        gvox, det = cpu_reference_sample(cfg, interp, target_s=per_step)
-        steps.append((gvox, det))
+    cores = len(os.sched_getaffinity(0))
+    # the whole --steps K --warmup W run is bounded: ~60 s of CPU compute split over the K steps
+    per_step = min(args.ref_seconds, max(0.5, 60.0 / max(1, args.steps)))
+    with mp.get_context("fork").Pool(cores) as pool:
+        for _ in range(max(args.warmup, args.warmup_ref)):
+            cpu_reference_sample(cfg, interp, target_s=min(0.5, per_step), cores=cores, pool=pool)
+        for _ in range(args.steps):
+            gvox, det = cpu_reference_sample(cfg, interp, target_s=per_step, cores=cores, pool=pool)
+            steps.append((gvox, det))
     gv = sorted(x[0] for x in steps)[len(steps) // 2]
     det = steps[-1][1]
     n, h, w = cfg["n"], cfg["h"], cfg["w"]
