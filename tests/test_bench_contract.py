@@ -39,3 +39,16 @@ def test_reference_arm_nonzero_ranks_exit_quietly():
             env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert not [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+
+
+def test_reference_arm_is_bounded_for_many_steps():
+    # the driver may pass a large --steps K: the per-step sample shrinks so the run stays short
+    import time
+
+    t0 = time.perf_counter()
+    r = run(["--impl", "reference", "--config", "1", "--steps", "40", "--warmup", "3"])
+    wall = time.perf_counter() - t0
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")][-1])
+    assert d["steps"] == 40 and d["value"] > 0
+    assert wall < 240, wall
