@@ -232,7 +232,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     from paper_2211_00645_b200 import _lib
     from paper_2211_00645_b200.deskew import deskew_device
-    from paper_2211_00645_b200.stream import StackStreamer, pinned_stack
+    from paper_2211_00645_b200.stream import StackStreamer, gpu_numa_cpus, near_gpu, pinned_stack
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -379,7 +379,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # streams) -> fused deskew on device -> projections D2H, every step
     e2e = None
     if not args.no_e2e:
-        host = pinned_stack(n, h, w)
+        host = pinned_stack(n, h, w, device=dev)
         host[:] = raw.cpu().numpy()
         streamer = StackStreamer(h, w, device=dev, chunk_frames=args.chunk_frames or None)
         out_host = {a: torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True) for a, t in projs.items()}
@@ -413,7 +413,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t[0])
         # the bound of this number: a plain pinned 256 MiB H2D copy on this box, measured now
-        probe_h = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+        with near_gpu(dev):
+            probe_h = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
         probe_d = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         probe_d.copy_(probe_h, non_blocking=True)
         a0.record(stream)
@@ -427,6 +428,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         e2e = {"value": world * vox / (e_ms * 1e-3) / 1e9, "unit": "GVoxels/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in projs.values()),
                "ms_per_step": e_ms, "h2d_gbs": h2d / (e_ms * 1e-3) / 1e9, "h2d_copy_ceiling_gbs": ceiling, "chunk_frames": streamer.chunk,
+               "pinned_on_gpu_numa_node": gpu_numa_cpus(dev) is not None,
                "path": "stream.StackStreamer.run (pinned host -> 2 copy streams -> ssb_deskew per chunk) + projections D2H; volume stays in HBM"}
 
     cpu = None
@@ -468,14 +470,14 @@ def run_stream(args, cfg, rank, world, local_rank):
     import torch
 
     from paper_2211_00645_b200 import _lib
-    from paper_2211_00645_b200.stream import StackStreamer, pinned_stack
+    from paper_2211_00645_b200.stream import StackStreamer, gpu_numa_cpus, near_gpu, pinned_stack
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     n, h, w = cfg["n"], cfg["h"], cfg["w"]
     s = native_shear(cfg["alpha"])
     u = canvas_rows(n, h, s)
-    host = pinned_stack(n, h, w)
+    host = pinned_stack(n, h, w, device=dev)
     host[:] = np.random.default_rng(rank).integers(0, 4096, size=(n, h, w), dtype=np.uint16)
     streamer = StackStreamer(h, w, device=dev, chunk_frames=args.chunk_frames or None)
     outs = {0: torch.empty((u, w), dtype=torch.uint16, pin_memory=True),
@@ -520,6 +522,7 @@ def run_stream(args, cfg, rank, world, local_rank):
             "data": "synthetic uniform [0,4096) in pinned host memory",
             "config": {"workload": cfg["name"], "interp": args.interp, "canvas": [u, w], "stacks_per_s": 1e3 / ms,
                        "latency_ms_last_chunk_to_host": lat, "chunk_frames": streamer.chunk, "tail_frames": streamer.tail,
+                       "pinned_on_gpu_numa_node": gpu_numa_cpus(dev) is not None,
                        "outputs": "XY/XZ/YZ max to host every stack, no volume",
                        "h2d_GBps": 2 * n * h * w / (ms * 1e-3) / 1e9},
             "gpu_launches": launches,

@@ -16,7 +16,9 @@ the projections accumulate on device (XY folds chunk after chunk with
 
 from __future__ import annotations
 
+import os
 import time
+from contextlib import contextmanager
 from dataclasses import dataclass
 
 import numpy as np
@@ -26,10 +28,58 @@ from .deskew import DeskewResult, canvas_rows_for, check_options, deskew_device,
 from .errors import ParameterError
 
 
-def pinned_stack(n: int, height: int, width: int) -> np.ndarray:
-    """(n, H, W) uint16 numpy array backed by page-locked host memory."""
+def _parse_cpulist(text: str) -> set:
+    cpus = set()
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        a, _, b = part.partition("-")
+        cpus.update(range(int(a), int(b or a) + 1))
+    return cpus
+
+
+def gpu_numa_cpus(device=None):
+    """Host CPUs of the GPU's NUMA node (sysfs, intersected with this thread's affinity), or
+    None when the platform does not say (single-node hosts, containers without sysfs)."""
+    try:
+        p = torch.cuda.get_device_properties(torch.device("cuda", torch.cuda.current_device())
+                                             if device is None else device)
+        pci = "/sys/bus/pci/devices/%04x:%02x:%02x.0/numa_node" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+        with open(pci) as f:
+            node = int(f.read())
+        if node < 0:
+            return None
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            cpus = _parse_cpulist(f.read()) & os.sched_getaffinity(0)
+        return cpus or None
+    except (OSError, ValueError, AttributeError, RuntimeError, AssertionError):
+        return None
+
+
+@contextmanager
+def near_gpu(device=None):
+    """Run the body on the GPU's NUMA node (this thread only, restored afterwards).
+
+    Page-locked buffers allocated inside land in that node's memory (local first-touch
+    policy), so the copy engines read them without crossing the socket link: on a
+    two-socket host a remote pinned stack copies at ~33 GB/s instead of ~55 GB/s."""
+    cpus = gpu_numa_cpus(device)
+    if cpus is None:
+        yield
+        return
+    old = os.sched_getaffinity(0)
+    os.sched_setaffinity(0, cpus)
+    try:
+        yield
+    finally:
+        os.sched_setaffinity(0, old)
+
+
+def pinned_stack(n: int, height: int, width: int, device=None) -> np.ndarray:
+    """(n, H, W) uint16 numpy array backed by page-locked host memory on ``device``'s NUMA node."""
     require_cuda()
-    t = torch.empty((n, height, width), dtype=torch.uint16, pin_memory=True)
+    with near_gpu(device):
+        t = torch.empty((n, height, width), dtype=torch.uint16, pin_memory=True)
     return t.numpy()  # the array's base holds the tensor: the pinned block lives as long as the array
 
 
@@ -98,8 +148,9 @@ class StackStreamer:
     def _staging_ring(self):
         if self._staging is None:
             shape = (self.chunk, self.height, self.width)
-            self._staging = [torch.empty(shape, dtype=torch.uint16, pin_memory=True)
-                             for _ in range(self.n_buffers)]
+            with near_gpu(self.device):
+                self._staging = [torch.empty(shape, dtype=torch.uint16, pin_memory=True)
+                                 for _ in range(self.n_buffers)]
         return self._staging
 
     def run(self, stack, shear_px: float, interp: str = "linear", *, formula: str = "canvas",
