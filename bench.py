@@ -8,10 +8,18 @@ config 2 = 512 frames x 2048 x 2048 uint16, 30 degree sheet, native shear
 (N, U, W) uint16 written + XY/XZ/YZ max projections.  Inputs (4.3 GB) and
 outputs (5.2 GB) are far larger than the 126 MB L2, so no flush is needed.
 
-Under torchrun (N > 1) every rank deskews its own stack per step (timelapse
-batch sharded by stack, config 4: weak scaling) and rank 0 gathers every
-rank's XY projection over NCCL (the display rank); the step time is the max
-over ranks of CUDA-event time.
+With ``--gpus N`` (N > 1) the bench runs config 4, the timelapse batch of 64
+distinct stacks sharded round-robin by stack over N ranks (one process per GPU,
+NCCL; weak scaling): a step deskews one stack per rank -- its next stack, held
+resident in HBM, content ``(base + 37 k) mod 4096`` for global stack k -- and
+gathers each stack's XY projection to rank 0 (the display rank) on a side
+stream, overlapped with the next stack's kernel.  The step time is the max over
+ranks of CUDA-event time.  Launched without torchrun, ``--gpus N`` re-executes
+itself under ``torch.distributed.run`` with N local ranks; the driver's own
+torchrun launch works the same way.  ``--config 5 --gpus N`` splits one long
+scan into scan-axis slabs merged with one NCCL reduce.  ``--dry-run --backend
+gloo`` exercises the N-rank launch, rendezvous, display gather and max-over-ranks
+timing on CPU (no kernels; value null).
 
 ``--impl reference`` times the reference's CPU algorithm (the oracle's numpy
 restatement of ProjectionCanvas.place + finalize_global, ss/pipeline.py:229-336,
@@ -39,6 +47,7 @@ CONFIGS = {
     1: dict(n=128, h=256, w=512, alpha=30.0, name="config1_128x256x512_30deg"),
     2: dict(n=512, h=2048, w=2048, alpha=30.0, name="config2_512x2048x2048_30deg"),
     3: dict(n=200, h=1024, w=1024, alpha=30.0, name="config3_200x1024x1024_30deg_live_stream"),
+    4: dict(n=512, h=2048, w=2048, alpha=30.0, name="config4_timelapse_64x512x2048x2048_30deg_by_stack", stacks=64),
     5: dict(n=8192, h=2048, w=2048, alpha=45.0, name="config5_8192x2048x2048_45deg_slabs_sum"),
 }
 PITCH = STEP = 0.115
@@ -63,6 +72,18 @@ def peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def lookup_traffic(n, h, w, interp, outputs, reduce):
+    """ncu DRAM bytes per launch of the dominant kernel for exactly this workload shape and
+    output set (profiles/traffic.json, keyed "NxHxW/interp/outputs/reduce"), else None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            table = json.load(f)
+    except (OSError, ValueError):
+        return None
+    v = table.get(f"{n}x{h}x{w}/{interp}/{outputs}/{reduce}")
+    return v.get("bytes") if isinstance(v, dict) else v
 
 
 def algorithmic_bytes(n, h, w, u, volume=True, axes=(0, 1, 2), reduce="max"):
@@ -194,10 +215,13 @@ def run_reference(args, cfg, rank, world):
     line = {
         "impl": "reference", "metric": "deskewed GVoxels/s (fused deskew+MIP)", "value": gv,
         "unit": "GVoxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": det["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        # one step = one full stack's worth of the reference's work, extrapolated from the sample
+        "ms_per_step": n * u * w / (gv * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u16 in / f64 lerp / u16 out", "data": "synthetic uniform [0,4096)",
-        "config": {"workload": cfg["name"], "interp": interp, "global_batch": 1, "seq_len": n,
-                   "stacks_per_s_equiv": 1e3 / det["ms_per_stack_equiv"], "canvas": [u, w]},
+        "config": {"workload": cfg["name"], "interp": interp, "shear_px": native_shear(cfg["alpha"]),
+                   "canvas": [u, w], "outputs": "XY max (ProjectionCanvas: the reference's only output)",
+                   "global_batch": 1, "seq_len": n, "stacks_per_s_equiv": gv * 1e9 / (n * u * w),
+                   "sample_ms": det["seconds"] * 1e3},
         "cpu_baseline": {"value": gv, "unit": "GVoxels/s", "cores": det["cores"], "kind": "port",
                          "sample": det["sample"]},
         "e2e": {"value": gv, "unit": "GVoxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -243,11 +267,34 @@ def run_ours(args, cfg, rank, world, local_rank):
     axes = (0, 1, 2)
     stream = torch.cuda.current_stream(dev)
 
-    # synthetic stack: config-4 rule, stack k = (base + 37 k) mod 4096, generated on device
+    # synthetic stacks, generated on device: global stack k = (base + 37 k) mod 4096.
+    # Config 2 (N = 1): stack 0, deskewed every step.  Config 4: this rank's shard of the
+    # timelapse (round-robin by stack, dist.shard_stacks), every stack distinct and resident in
+    # HBM when it fits (64 stacks over 2 ranks = 137 GB per rank), else as many as fit, cycled.
     g = torch.Generator(device=dev).manual_seed(1234)
-    base = torch.randint(0, 4096, (n, h, w), generator=g, device=dev, dtype=torch.int32)
-    raw = ((base + 37 * rank) % 4096).to(torch.uint16)
+    base = torch.randint(0, 4096, (n, h, w), generator=g, device=dev, dtype=torch.int16)
+
+    def make_stack(k):
+        out = torch.empty_like(base)
+        for f0 in range(0, n, 64):  # 64-frame pieces: no stack-sized temporaries
+            torch.remainder(base[f0:f0 + 64] + (37 * k) % 4096, 4096, out=out[f0:f0 + 64])
+        return out.view(torch.uint16)
+
+    timelapse = "stacks" in cfg
+    if timelapse:
+        from paper_2211_00645_b200 import dist as D
+
+        mine = D.shard_stacks(cfg["stacks"], rank, world)
+        stack_bytes = 2 * n * h * w
+        free = torch.cuda.mem_get_info(dev)[0]
+        # room for the volume, the projections, the e2e staging and a margin
+        fit = max(1, int((free - 2 * n * u * w - stack_bytes - (12 << 30)) // stack_bytes))
+        raws = [make_stack(k) for k in mine[:min(len(mine), fit)]]
+    else:
+        mine = [rank]
+        raws = [make_stack(rank)]
     del base
+    raw = raws[0]
     vol = torch.empty((n, u, w), dtype=torch.uint16, device=dev)
     projs = {0: torch.empty((u, w), dtype=torch.uint16, device=dev),
              1: torch.empty((n, w), dtype=torch.uint16, device=dev),
@@ -263,12 +310,13 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     def step():
         b = counter[0] % len(xy_bufs)
+        stack = raws[counter[0] % len(raws)]  # this rank's next stack of the timelapse
         counter[0] += 1
         if pending[b] is not None:
             with torch.cuda.stream(stream):
                 pending[b].wait()  # the gather that read this buffer has finished
             pending[b] = None
-        deskew_device(raw, s, interp, reduce=reduce, volume=vol, projections={0: xy_bufs[b], 1: projs[1], 2: projs[2]},
+        deskew_device(stack, s, interp, reduce=reduce, volume=vol, projections={0: xy_bufs[b], 1: projs[1], 2: projs[2]},
                       stream=stream)
         if world > 1 and not overlap:
             dist.gather(xy_bufs[b].view(torch.uint8), gather, dst=0)
@@ -386,13 +434,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     bytes_launch = algorithmic_bytes(n, h, w, u, True, axes, reduce)
     peak, peak_kind = peaks()
     achieved = bytes_launch / (kern_avg * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(cfg["name"])
-        except Exception:
-            traffic = None
+    traffic = lookup_traffic(n, h, w, interp, "volume+xy,xz,yz", reduce)
 
     # end-to-end through the public streaming API: pinned host stack -> H2D (2 copy
     # streams) -> fused deskew on device -> projections D2H, every step
@@ -461,10 +503,14 @@ def run_ours(args, cfg, rank, world, local_rank):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u16 in / f64 lerp / u16 out", "data": "synthetic uniform [0,4096), generated on device",
-            "config": {"workload": cfg["name"] + (" x1 stack per GPU (config 4 timelapse sharding)" if world > 1 else ""),
-                       "interp": interp, "shear_px": s, "canvas": [u, w], "outputs": "volume (N,U,W) u16 + XY/XZ/YZ max",
-                       "stacks_per_s": world * 1e3 / ms, "global_batch": world, "seq_len": n,
-                       "parallelism": f"dp{world} (stacks)", "l2": l2_note},
+            "config": {"workload": cfg["name"], "interp": interp, "shear_px": s, "canvas": [u, w],
+                       "outputs": "volume (N,U,W) u16 + XY/XZ/YZ max", "stacks_per_s": world * 1e3 / ms,
+                       "global_batch": world, "seq_len": n, "parallelism": f"dp{world} (stacks)", "l2": l2_note,
+                       **({"stacks_total": cfg["stacks"], "stacks_per_rank": len(mine),
+                           "resident_distinct_stacks_per_rank": len(raws),
+                           "step": "one stack per rank (its next stack of the shard); XY gathered to rank 0 "
+                                   "over NCCL on a side stream, overlapped with the next stack"}
+                          if timelapse else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "spec_peak": SPEC_HBM_GBS, "frac_of_spec": achieved / SPEC_HBM_GBS,
@@ -620,13 +666,62 @@ def run_slabs(args, cfg, rank, world, local_rank):
         }), flush=True)
 
 
+def run_dry(args, cfg, rank, world, local_rank):
+    """N-rank plumbing without kernels (CPU test of the multi-GPU launch): rendezvous over the
+    chosen backend, per step the display gather of a small uint16 XY tile (dist.gather_to_display,
+    the config-4 merge), timing as max over ranks.  Prints the contract line with value null."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2211_00645_b200 import dist as D
+
+    xy = torch.full((64, 64), rank + 1, dtype=torch.uint16)
+    got = None
+    for _ in range(args.warmup):
+        got = D.gather_to_display(xy)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        got = D.gather_to_display(xy)
+    dist.barrier()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    t = torch.tensor([ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ok = got is not None and [int(g[0, 0]) for g in got] == list(range(1, world + 1))
+        print(json.dumps({
+            "metric": "deskewed GVoxels/s (fused deskew+MIP)", "value": None, "unit": "GVoxels/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(t[0]), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "none (dry run)", "dry_run": True,
+            "config": {"workload": cfg["name"], "backend": args.backend, "parallelism": f"dp{world} (stacks)",
+                       "stacks_per_rank": len(D.shard_stacks(cfg.get("stacks", world), rank, world)),
+                       "display_gather_ok": ok}}), flush=True)
+
+
+def self_launch(n: int) -> int:
+    """Re-execute this command under torch.distributed.run with n local ranks (one per GPU)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nRanks) stay visible
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
+                    help="default: 2 at one GPU, 4 (timelapse by stack) at N > 1")
     ap.add_argument("--interp", default="linear", choices=["linear", "nearest"])
     ap.add_argument("--heat-seconds", type=float, default=1.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -637,22 +732,42 @@ def main():
                     help="N > 1: gather each step's XY before the next deskew instead of overlapping")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunk-frames", type=int, default=0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--dry-run", action="store_true", help="N-rank launch/gather/timing plumbing only (no kernels)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        if not args.dry_run:
+            import torch
+
+            if torch.cuda.device_count() < args.gpus:
+                sys.exit(f"bench.py: --gpus {args.gpus} but {torch.cuda.device_count()} CUDA devices visible")
+        sys.exit(self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = 2 if max(world, args.gpus) == 1 else 4
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
-        run_reference(args, cfg, rank, world)
+        run_reference(args, cfg, rank, world if "WORLD_SIZE" in os.environ else args.gpus)
+        return
+    if args.dry_run:
+        import torch.distributed as dist
+
+        dist.init_process_group(args.backend)
+        try:
+            run_dry(args, cfg, rank, world, local_rank)
+        finally:
+            dist.destroy_process_group()
         return
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.init_process_group(args.backend, device_id=torch.device("cuda", local_rank))
     try:
         runner = {3: run_stream, 5: run_slabs}.get(args.config, run_ours)
         runner(args, cfg, rank, world, local_rank)

@@ -64,20 +64,28 @@ __host__ __device__ constexpr int box_slack() {
 #ifndef SSB_L2_PROMO  // A/B knob: L2 promotion of the TMA box loads
 #define SSB_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_128B
 #endif
+#ifndef SSB_REGULAR_STAGES
+#define SSB_REGULAR_STAGES 1  // A/B knob: 0 = per-row tables for every stage
+#endif
 #ifndef SSB_YZ_LIVE_ONLY
 #define SSB_YZ_LIVE_ONLY 1  // A/B knob (profiles/README.md)
 #endif
-template <int ROWS>
+#ifndef SSB_XY_STAGES
+#define SSB_XY_STAGES 6  // ring depth of 4-row kernels without XZ staging (A/B knob)
+#endif
+template <int ROWS, bool SIDE = true>
 struct Cfg {
     static constexpr int kRows = ROWS;
     static constexpr int kTU = kConsumerWarps * ROWS;
     static constexpr int kBoxRows = kTU + 4;
-    static constexpr int kStages = ROWS >= 8 ? 3 : 5;
+    // without side projections the XZ staging buffer is not needed and a deeper ring fits
+    static constexpr int kStages = ROWS >= 8 ? 3 : (SIDE ? 5 : SSB_XY_STAGES);
     static constexpr int kXzBatch = ROWS >= 8 ? 1 : 2;  // max-mode slices per XZ barrier
     static constexpr int kRowWords = (kTU + 31) / 32;   // 32-row groups the producer lanes cover
     // XZ staging: max mode packs u16x2 (kTX/2 words per warp and slice); sum mode (ROWS 4) u32
-    static constexpr int kXzWords = ROWS >= 8 ? 2 * kXzBatch * kConsumerWarps * (kTX / 2)
-                                              : 2 * kConsumerWarps * kTX;
+    static constexpr int kXzWords = !SIDE ? 4
+                                    : ROWS >= 8 ? 2 * kXzBatch * kConsumerWarps * (kTX / 2)
+                                                : 2 * kConsumerWarps * kTX;
     template <int INTERP, int FORMULA>
     static constexpr int box_rows() {
         return kTU + 2 * box_slack<INTERP, FORMULA>();
@@ -88,15 +96,33 @@ struct Cfg {
 // Sampling parameters of one canvas row for one slice (written by the producer).
 // Rows outside the slice's span point both taps at a shared zero row with weights
 // (1, 0), which yields exactly 0 -- the consumer loop has no per-row branches.
+//
+// Every linear voxel is rint(E) with E the reference's fp64 expression, and E lies within
+// 2^-34.5 of a + w*(b - a) for the row weight w (canvas: w = f; npinterp: w = t/dx).  The
+// consumers evaluate rint(a + w*(b - a)) in fp32 twice, with w rounded down (w_lo <= w - 2^-33)
+// and up (w_hi >= w + 2^-33): one FFMA on 2^23 + a rounds to the integer grid exactly once, ties
+// to even.  E lies between the two (monotone in w), so where both round to the same integer
+// that integer is rint(E); the rare lanes where they differ (a half-integer inside the bracket:
+// about 2^-23 |b - a| of the voxels) recompute their 8 voxels with the exact fp64 expression.
 struct alignas(16) RowP {
-    double c0;       // canvas: w0 = 1-f       npinterp: t
-    double c1;       // canvas: f              npinterp: dx
-    double n0;       // -c0 * 2^52
-    double n1;       // -c1 * 2^52
     uint32_t off_a;  // shared-memory byte address of tap a (row j0)
     uint32_t off_b;  // tap b (row j1)
     int32_t kind;    // npinterp only: 3 = dx == 1 (incl. copies, t = 0), 2 = general dx
     int32_t pad;
+    float w_lo, w_lo2, w_hi, w_hi2;  // fp32 bracket of the row weight, duplicated for f32x2 ops
+    double c0;       // canvas: w0 = 1-f       npinterp: t
+    double c1;       // canvas: f              npinterp: dx
+};
+
+// A regular stage: every row of the tile lies inside the slice's span and the output window,
+// its taps are unclamped (tap a of tile row r is frame row j0 + r, tap b the next one) and one
+// fp32 bracket holds every row's weight (canvas formula; nearest copies row j0 + r).  About 94 % of
+// the stages of a 2048-row frame; the producer then writes these 24 bytes instead of a row table.
+struct alignas(16) StageP {
+    double off;    // i*s of the slice (the fallback re-derives each row's exact weight from it)
+    float w_lo, w_hi;
+    int32_t a0;    // box row of tap a of tile row 0
+    int32_t j0;    // frame row of tap a of tile row 0
 };
 
 struct Params {
@@ -134,14 +160,16 @@ __host__ __device__ constexpr int smem_ac() {
     return AC <= 4 ? AC : 16;
 }
 
-template <int ROWS, int AC = 16>
+template <int ROWS, int AC = 16, bool SIDE = true>
 struct Smem {
-    using C = Cfg<ROWS>;
+    using C = Cfg<ROWS, SIDE>;
     uint16_t box[C::kStages][C::kBoxRows][row_pitch<AC>()];
     uint16_t zero_row[kTX + 8];
     RowP rows[C::kStages][C::kTU];
     uint32_t hdr[C::kStages];  // bit 16: slice touches the tile; bits 0..14: warps with live rows;
-                               // bits 17..31: warps whose rows chain their taps
+                               // bits 17..31: warps whose rows chain their taps; bit 15: regular
+                               // stage (taps and weights from sp[], the row table is not written)
+    StageP sp[C::kStages];
     alignas(16) uint32_t xz[C::kXzWords];
     uint64_t full[C::kStages];
     uint64_t empty[C::kStages];
@@ -230,112 +258,77 @@ __device__ __forceinline__ uint32_t voxel(uint32_t a, uint32_t b, const double c
     }
 }
 
+// Exact fp64 evaluation of 8 voxels (the fallback of the fp32 bracket, see RowP): returns them
+// as 2^23-biased fp32 bit patterns (0x4B000000 | v), the fast path's representation.
 template <int FORMULA>
-__device__ __forceinline__ uint4 voxels8(const uint4 a, const uint4 b, const RowP &rp) {
-    const double c0 = rp.c0, c1 = rp.c1, n0 = rp.n0, n1 = rp.n1;
-    const int kind = FORMULA == SSB_FORMULA_CANVAS ? 2 : rp.kind;
+__device__ __forceinline__ void exact8(const uint4 a, const uint4 b, const double c0, const double c1, const int kind_,
+                                       uint32_t (&bits)[8]) {
+    const double n0 = __dmul_rn(c0, -kTwo52), n1 = __dmul_rn(c1, -kTwo52);  // exact
+    const int kind = FORMULA == SSB_FORMULA_CANVAS ? 2 : kind_;
     const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
     const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
-    uint32_t o[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const uint32_t lo = voxel<FORMULA>(aw[q] & 0xFFFFu, bw[q] & 0xFFFFu, c0, c1, n0, n1, kind);
-        const uint32_t hi = voxel<FORMULA>(aw[q] >> 16, bw[q] >> 16, c0, c1, n0, n1, kind);
-        o[q] = __byte_perm(lo, hi, 0x5410);
+        bits[2 * q] = 0x4B000000u | voxel<FORMULA>(aw[q] & 0xFFFFu, bw[q] & 0xFFFFu, c0, c1, n0, n1, kind);
+        bits[2 * q + 1] = 0x4B000000u | voxel<FORMULA>(aw[q] >> 16, bw[q] >> 16, c0, c1, n0, n1, kind);
     }
-    return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-// Tap conversion for the chained canvas path (SSB_CVT_MODE):
-//   0  2^52 trick for every tap value: integer extract + constant high word, DFMA with -w*2^52;
-//   1  native I2F.F64 for every value (one conversion-pipe op, ~16/clk/SM on B200) + DMUL;
-//   2  mixed: low halves native (I2F.F64.U16 reads the half in place, no extract), high halves
-//      by the trick -- 1.5 issue slots per value and half the conversion-pipe load of mode 1.
-// All three give fl(w*a) exactly.  Measured on B200 (profiles/README.md): mode 2 is 2.6-3.4 %
-// faster than mode 0 projection-only and equal with a volume; mode 1 is slowest (conversion pipe).
-#ifndef SSB_CVT_MODE
-#define SSB_CVT_MODE 2
-#endif
-template <int C>
-__device__ __forceinline__ constexpr bool native_tap() {
-    return SSB_CVT_MODE == 1 || (SSB_CVT_MODE == 2 && (C & 1) == 0);
-}
+constexpr uint32_t kBias = 0x4B000000u;  // fp32 bits of 2^23: a voxel v is carried as kBias | v
 
-// I2F.F64.U16 of the low half of a 32-bit register (no separate extract)
-__device__ __forceinline__ double u16lo_to_f64(uint32_t w) {
-    double r;
-    asm("cvt.rn.f64.u16 %0, %1;" : "=d"(r) : "h"((unsigned short)w));
+// ---- fp32x2 (FFMA2 / FADD2) helpers: a 64-bit register pair holds two fp32 lanes
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 f2pack(uint32_t lo, uint32_t hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
     return r;
 }
 
-__device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
+__device__ __forceinline__ void f2unpack(f32x2 v, uint32_t &lo, uint32_t &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
+
+__device__ __forceinline__ f32x2 f2sub(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+__device__ __forceinline__ f32x2 f2fma(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+
+// 8 packed pixels -> 4 fp32 pairs holding 2^23 + pixel (one PRMT per pixel: 0x4B00 | pixel)
+__device__ __forceinline__ void to_f23(const uint4 t, f32x2 (&o)[4]) {
     const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = f2pack(__byte_perm(w4[q], 0x4B00u, 0x5410), __byte_perm(w4[q], 0x4B00u, 0x5432));
+}
+
+// rint(a + w*(b - a)) for 8 voxels at both ends of the weight bracket; bits = the w_lo results as
+// 2^23-biased fp32 bit patterns.  Returns nonzero iff some voxel's two results differ.
+__device__ __forceinline__ uint32_t lerp8_f32(const f32x2 (&A)[4], const f32x2 (&B)[4], const f32x2 wlo,
+                                              const f32x2 whi, uint32_t (&bits)[8]) {
+    uint32_t chk = 0;
+#pragma unroll
     for (int q = 0; q < 4; ++q) {
-        o[2 * q] = (SSB_CVT_MODE != 0) ? u16lo_to_f64(w4[q]) : biased(w4[q] & 0xFFFFu);
-        o[2 * q + 1] = (SSB_CVT_MODE == 1) ? __uint2double_rn(w4[q] >> 16) : biased(w4[q] >> 16);
+        const f32x2 d = f2sub(B[q], A[q]);  // b - a, exact
+        const f32x2 lo = f2fma(wlo, d, A[q]);
+        const f32x2 hi = f2fma(whi, d, A[q]);
+        uint32_t x0, x1;
+        f2unpack(f2sub(hi, lo), x0, x1);  // 0 or +-1 per voxel
+        chk |= x0 | x1;
+        f2unpack(lo, bits[2 * q], bits[2 * q + 1]);
     }
-}
-
-template <int C>
-__device__ __forceinline__ double tap_prod(double c, double a, double n) {
-    if (native_tap<C>()) return __dmul_rn(c, a);
-    return __fma_rn(c, a, n);
-}
-
-// canvas lerp of 8 voxels from converted taps: rint(fl(fl(w0*a) + fl(f*b))) as 8 u32 values
-template <int C>
-__device__ __forceinline__ uint32_t lerp_one(const double a, const double b, const double c0, const double c1,
-                                             const double n0, const double n1) {
-    return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(tap_prod<C>(c0, a, n0), tap_prod<C>(c1, b, n1)), kRintMagic));
-}
-
-// np.interp with dx == 1 (phantom.reference_deskew, ss/phantom.py:396-402) from converted
-// taps: slope = b - a exactly, v = rint(fl(fl(slope * t) + a)); biased taps are unbiased by an
-// exact subtraction (their difference is exact either way)
-template <int C>
-__device__ __forceinline__ uint32_t np_one(const double a, const double b, const double t) {
-    const double av = native_tap<C>() ? a : __dsub_rn(a, kTwo52);
-    const double prod = __dmul_rn(__dsub_rn(b, a), t);  // == sign(d) * fl(|d| * t)
-    return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(prod, av), kRintMagic));
-}
-
-__device__ __forceinline__ void np_biased8_raw(const double (&a)[8], const double (&b)[8], const double t,
-                                               uint32_t (&r)[8]) {
-    r[0] = np_one<0>(a[0], b[0], t);
-    r[1] = np_one<1>(a[1], b[1], t);
-    r[2] = np_one<2>(a[2], b[2], t);
-    r[3] = np_one<3>(a[3], b[3], t);
-    r[4] = np_one<4>(a[4], b[4], t);
-    r[5] = np_one<5>(a[5], b[5], t);
-    r[6] = np_one<6>(a[6], b[6], t);
-    r[7] = np_one<7>(a[7], b[7], t);
-}
-
-__device__ __forceinline__ void lerp_biased8_raw(const double (&a)[8], const double (&b)[8], const double c0,
-                                                 const double c1, const double n0, const double n1,
-                                                 uint32_t (&r)[8]) {
-    r[0] = lerp_one<0>(a[0], b[0], c0, c1, n0, n1);
-    r[1] = lerp_one<1>(a[1], b[1], c0, c1, n0, n1);
-    r[2] = lerp_one<2>(a[2], b[2], c0, c1, n0, n1);
-    r[3] = lerp_one<3>(a[3], b[3], c0, c1, n0, n1);
-    r[4] = lerp_one<4>(a[4], b[4], c0, c1, n0, n1);
-    r[5] = lerp_one<5>(a[5], b[5], c0, c1, n0, n1);
-    r[6] = lerp_one<6>(a[6], b[6], c0, c1, n0, n1);
-    r[7] = lerp_one<7>(a[7], b[7], c0, c1, n0, n1);
+    return chk;
 }
 
 __device__ __forceinline__ uint4 pack8(const uint32_t (&r)[8]) {
     return make_uint4(__byte_perm(r[0], r[1], 0x5410), __byte_perm(r[2], r[3], 0x5410),
                       __byte_perm(r[4], r[5], 0x5410), __byte_perm(r[6], r[7], 0x5410));
-}
-
-// ... and packed 8 x uint16
-__device__ __forceinline__ uint4 lerp_biased8(const double (&a)[8], const double (&b)[8], const double c0,
-                                              const double c1, const double n0, const double n1) {
-    uint32_t r[8];
-    lerp_biased8_raw(a, b, c0, c1, n0, n1, r);
-    return pack8(r);
 }
 
 template <bool kMax>
@@ -443,6 +436,14 @@ __device__ __forceinline__ uint32_t redux_add(uint32_t v) {
     return r;
 }
 
+// fp32 bracket [w_lo, w_hi] of the row weight w with a 2^-33 margin on either side: wider than the
+// 2^-34.5 between the reference's fp64 result and a + w*(b - a) for any |b - a| >= 1
+__device__ __forceinline__ void set_bracket(RowP &o, double w) {
+    constexpr double kMargin = 1.1641532182693481e-10;  // 2^-33
+    o.w_lo = o.w_lo2 = __double2float_rd(__dsub_rn(w, kMargin));
+    o.w_hi = o.w_hi2 = __double2float_ru(__dadd_rn(w, kMargin));
+}
+
 // Row table entry of canvas row u for one slice (producer lanes).  Returns whether
 // the row is live (inside the window and the slice's span).
 // Row-copy mode: frame row j of the slice sits at byte (d0 + 2*j*rs) & 15 of its slot (d0: the
@@ -453,15 +454,11 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
                                          uint32_t zero_addr, uint32_t d0, uint32_t rs2) {
     o.c0 = 1.0;
     o.c1 = 0.0;
-    o.n0 = -kTwo52;
-    o.n1 = -0.0;
     o.off_a = o.off_b = zero_addr;
     o.kind = 3;
     o.pad = 0;
-    if (FORMULA == SSB_FORMULA_NPINTERP) {
-        o.c0 = 0.0;  // t = 0: copy of tap a (the zero row)
-        o.n0 = -0.0;
-    }
+    if (FORMULA == SSB_FORMULA_NPINTERP) o.c0 = 0.0;  // t = 0: copy of tap a (the zero row)
+    set_bracket(o, 0.0);
     if (!in_window || u < lo || u > hi) return false;
     const RowParam rp = row_param<INTERP, FORMULA>(u, lo, off, h);
     // the box covers [box_r0, box_r0 + TU + 2*slack): a tap outside it would read another
@@ -473,9 +470,9 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     if (rp.kind >= 2) {
         o.c0 = rp.c0;
         o.c1 = rp.c1;
-        o.n0 = -(rp.c0 * kTwo52);  // exact: power-of-two scaling
-        o.n1 = -(rp.c1 * kTwo52);
         o.kind = rp.kind;
+        // weight of a + w*(b - a): canvas f; np.interp t (dx == 1) or t/dx
+        set_bracket(o, FORMULA == SSB_FORMULA_CANVAS ? rp.c1 : rp.kind == 3 ? rp.c0 : __ddiv_rn(rp.c0, rp.c1));
     } else if (FORMULA == SSB_FORMULA_CANVAS) {
         // copy (only reachable for h == 1 paths): w0 = 1, f = 0
         o.off_b = o.off_a;
@@ -491,8 +488,11 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
 // take the u32 voxels straight from the rint, no pack/unpack: measured 2-5 % faster).
 // Row-copy mode (AC < 16), !FULL: a lane may straddle the right edge (nv < 8 pixels inside); its
 // outside pixels are zeroed before any reduction and never stored.
-template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN, int AC>
-__device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off,
+// REG: a regular stage (StageP): taps at fixed box rows (tap_base + k rows), one weight bracket,
+// the fallback re-derives row k's exact weight from the slice offset (canvas row u0 + k, tap j0 + k).
+template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN, int AC, bool REG>
+__device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off, const uint32_t tap_base,
+                                          const StageP &sp, const int64_t u0,
                                           uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
                                           const int nv, uint4 (&acc_max)[ROWS],
                                           uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
@@ -502,7 +502,11 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     constexpr bool kPairXz = kMax && SIDE && kStream;   // XZ over row pairs with 3-input maxes
     uint4 xz_prev = make_uint4(0, 0, 0, 0);
     const bool store = vrow != nullptr;
-    constexpr bool chain = CHAIN && INTERP == SSB_INTERP_LINEAR;
+    constexpr bool chain = (CHAIN || REG) && INTERP == SSB_INTERP_LINEAR;
+    constexpr uint32_t kPitch = 2u * row_pitch<AC>();
+    // tap addresses of row k (lane offset included)
+    auto tap_a = [&](const int k) { return REG ? tap_base + (uint32_t)k * kPitch : rg[k].off_a + lane_off; };
+    auto tap_b = [&](const int k) { return REG ? tap_base + (uint32_t)(k + 1) * kPitch : rg[k].off_b + lane_off; };
     constexpr bool kEdge = AC != 16 && !FULL;  // a lane may straddle the right edge
     auto put = [&](const int k, const uint4 v) {
         if (!(store && (FULL || (k < rows_ok && col_ok)))) return;
@@ -539,46 +543,71 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         }
     };
     uint4 vs[kStream ? 1 : ROWS];
-    double prev[8];
-    if (chain) to_biased8(lds8<smem_ac<AC>()>(rg[0].off_a + lane_off), prev);
+    f32x2 prev[4];
+    if (chain) to_f23(lds8<smem_ac<AC>()>(tap_a(0)), prev);
+    f32x2 wlo_s = 0, whi_s = 0;
+    if (REG) {
+        wlo_s = f2pack(__float_as_uint(sp.w_lo), __float_as_uint(sp.w_lo));
+        whi_s = f2pack(__float_as_uint(sp.w_hi), __float_as_uint(sp.w_hi));
+    }
 #pragma unroll
     for (int k = 0; k < ROWS; ++k) {
         uint4 v;
         if (INTERP == SSB_INTERP_NEAREST) {
-            v = lds8<smem_ac<AC>()>(rg[k].off_a + lane_off);
-        } else if (chain) {
-            // chained taps: tap row k+1 is tap b of row k and tap a of row k+1
-            double cur[8];
-            to_biased8(lds8<smem_ac<AC>()>(rg[k].off_b + lane_off), cur);
-            uint32_t r[8];
-            if (FORMULA == SSB_FORMULA_NPINTERP) np_biased8_raw(prev, cur, rg[k].c0, r);
-            else lerp_biased8_raw(prev, cur, rg[k].c0, rg[k].c1, rg[k].n0, rg[k].n1, r);
-            if (!kMax && kStream) {
-                // sums take the rounded voxels straight from the rint trick (no unpacking)
+            v = lds8<smem_ac<AC>()>(tap_a(k));
+        } else {
+            // fp32 bracket of the lerp (RowP); chained taps: tap row k+1 is tap b of row k and
+            // tap a of row k+1, converted once
+            f32x2 A[4], B[4];
+            to_f23(lds8<smem_ac<AC>()>(tap_b(k)), B);
+            if (chain) {
 #pragma unroll
-                for (int c = 0; c < 8; ++c) prev[c] = cur[c];
-                if (kEdge) {
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) r[c] = c < nv ? r[c] : 0u;
+                for (int q = 0; q < 4; ++q) A[q] = prev[q];
+            } else {
+                to_f23(lds8<smem_ac<AC>()>(tap_a(k)), A);
+            }
+            f32x2 wlo = wlo_s, whi = whi_s;
+            if (!REG) {
+                const uint4 wq = *reinterpret_cast<const uint4 *>(&rg[k].w_lo);
+                wlo = f2pack(wq.x, wq.y);
+                whi = f2pack(wq.z, wq.w);
+            }
+            uint32_t bits[8];
+            if (lerp8_f32(A, B, wlo, whi, bits) != 0) {
+                const uint4 ta = lds8<smem_ac<AC>()>(tap_a(k)), tb = lds8<smem_ac<AC>()>(tap_b(k));
+                if (REG) {
+                    // canvas formula, unclamped taps j0+k, j0+k+1: f = fl(fl(u - off) - j0), w0 = 1 - f
+                    const double f = __dsub_rn(__dsub_rn((double)(u0 + k), sp.off), (double)(sp.j0 + k));
+                    exact8<FORMULA>(ta, tb, __dsub_rn(1.0, f), f, 2, bits);
+                } else {
+                    exact8<FORMULA>(ta, tb, rg[k].c0, rg[k].c1, rg[k].kind, bits);
                 }
-                put(k, pack8(r));
+            }
+            if (chain) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) prev[q] = B[q];
+            }
+            if (!kMax && kStream) {
+                // sums add the 2^23-biased bits as they are (mod 2^32): the caller removes the
+                // bias once per pass (XZ), per item (XY: live passes x kBias); a YZ row sums 256
+                // biased values, whose bias is 0 mod 2^32.  Masked columns carry the bare bias.
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (kEdge && c >= nv) bits[c] = kBias;
+                put(k, pack8(bits));
                 uint32_t rs = 0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    acc_sum[k][c] += r[c];
+                    acc_sum[k][c] += bits[c];
                     if (SIDE) {
-                        xz_sum[c] += r[c];
-                        rs += r[c];
+                        xz_sum[c] += bits[c];
+                        rs += bits[c];
                     }
                 }
                 if (SIDE) yzv[k] = redux_add(rs);
                 continue;
             }
-            v = pack8(r);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) prev[c] = cur[c];
-        } else {
-            v = voxels8<FORMULA>(lds8<smem_ac<AC>()>(rg[k].off_a + lane_off), lds8<smem_ac<AC>()>(rg[k].off_b + lane_off), rg[k]);
+            v = pack8(bits);
         }
         if (kStream) consume(k, v);
         else vs[k] = kEdge ? mask_cols(v, nv) : v;
@@ -597,12 +626,12 @@ template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
 __global__ void __launch_bounds__(kThreads, 1)
     deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
-    using C = Cfg<ROWS>;
+    using C = Cfg<ROWS, SIDE>;
     constexpr int kTU = C::kTU;
     constexpr int kStages = C::kStages;
     constexpr int kXzBatch = kMax ? C::kXzBatch : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem<ROWS, AC> &sm = *reinterpret_cast<Smem<ROWS, AC> *>(smem_raw);
+    Smem<ROWS, AC, SIDE> &sm = *reinterpret_cast<Smem<ROWS, AC, SIDE> *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
@@ -739,6 +768,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+                // regular stage (StageP): the tile lies inside the span and the window and, for the
+                // canvas lerp, RN(u - off) = u - base - 1 + (1 - phi) +- 2^-31 for every row (phi =
+                // frac(off) away from 0 and 1 by 2^-30, |u - off| < 2^20): taps j0 + r, j0 + r + 1
+                // unclamped and f = 1 - phi within (H + 2) * 2^-52
+                bool regular = false;
+                if (AC == 16 && FORMULA == SSB_FORMULA_CANVAS && hit && SSB_REGULAR_STAGES &&
+                    (int64_t)(ut + 1) * kTU <= p.u_count && lo <= tu0 && tu0 + kTU - 1 <= hi && p.h < (1 << 20)) {
+                    StageP spv;
+                    spv.off = off;
+                    if (INTERP == SSB_INTERP_NEAREST) {
+                        regular = true;
+                        spv.a0 = (int32_t)(tu0 - lo - box_r0);  // = 0
+                        spv.j0 = (int32_t)(tu0 - lo);
+                        spv.w_lo = spv.w_hi = 0.f;
+                    } else {
+                        const double phi = __dsub_rn(off, floor(off));  // exact (off >= 0)
+                        const bool int_off = phi == 0.0;
+                        const int64_t j0 = tu0 - base - (int_off ? 0 : 1);
+                        if ((int_off || (phi > 0x1p-30 && phi < 1.0 - 0x1p-30)) && j0 >= 0 && j0 + kTU <= p.h - 1) {
+                            regular = true;
+                            const double f = int_off ? 0.0 : __dsub_rn(1.0, phi);
+                            const double m = __dadd_rn(1.1641532182693481e-10, __dmul_rn((double)(p.h + 2), 0x1p-52));
+                            spv.w_lo = __double2float_rd(__dsub_rn(f, m));
+                            spv.w_hi = __double2float_ru(__dadd_rn(f, m));
+                            spv.a0 = (int32_t)(j0 - box_r0);
+                            spv.j0 = (int32_t)j0;
+                        }
+                    }
+                    if (regular && lane == 0) {
+                        sm.sp[stage] = spv;
+                        sm.hdr[stage] = 0x7FFFu | (1u << 15) | (1u << 16) | (0x7FFFu << 17);
+                    }
+                }
+                if (!regular) {
                 uint32_t live[C::kRowWords];
 #pragma unroll
                 for (int j = 0; j < C::kRowWords; ++j) live[j] = 0;
@@ -770,15 +833,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         chained = true;
 #pragma unroll
                         for (int k = 0; k + 1 < ROWS; ++k) chained &= g[k].off_b == g[k + 1].off_a;
-                        if (FORMULA == SSB_FORMULA_NPINTERP) {  // np.interp: dx == 1 rows only
-#pragma unroll
-                            for (int k = 0; k < ROWS; ++k) chained &= g[k].kind == 3;
-                        }
                     }
                 }
                 const uint32_t any_mask = __ballot_sync(0xffffffffu, any);
                 const uint32_t chain_mask = __ballot_sync(0xffffffffu, chained);
                 if (lane == 0) sm.hdr[stage] = any_mask | (hit ? (1u << 16) : 0u) | (chain_mask << 17);
+                }
                 __syncwarp();
                 mbar_arrive(&sm.full[stage]);
                 if (++stage == kStages) { stage = 0; sphase ^= 1; }
@@ -831,10 +891,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         const int ns = (int)(s_end - s_begin);
+        // linear sums carry 2^23-biased voxels (rows_pass): bias to remove per live pass
+        constexpr bool kBiased = !kMax && INTERP == SSB_INTERP_LINEAR;
+        uint32_t n_live = 0;
         for (int si = 0; si < ns; ++si) {
             mbar_wait(&sm.full[stage], sphase);
             const uint32_t hdr = sm.hdr[stage];
             const bool live = (hdr >> 16) & (hdr >> warp) & 1u;
+            n_live += live ? 1u : 0u;
             uint4 xz_max = make_uint4(0, 0, 0, 0);
             uint32_t xz_sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             uint32_t yzv[ROWS];
@@ -843,26 +907,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (live) {
                 const RowP *rg = &sm.rows[stage][warp * ROWS];
                 const bool chained = (hdr >> (17 + warp)) & 1u;
-                // four specialisations so the row loop has no per-row branches
-                if (fast) {
-                    if (chained)
-                        rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE, true, AC>(rg, lane_off, vrow, p.w, rows_ok,
-                                                                                col_ok, nv, acc_max, acc_sum, xz_max,
-                                                                                xz_sum, yzv);
-                    else
-                        rows_pass<INTERP, FORMULA, kMax, true, ROWS, SIDE, false, AC>(rg, lane_off, vrow, p.w, rows_ok,
-                                                                                 col_ok, nv, acc_max, acc_sum, xz_max,
-                                                                                 xz_sum, yzv);
+                const int64_t u0 = p.u_begin + r0;  // canvas row of this warp's row 0
+#define SSB_ROWS_PASS(F, CH, RG)                                                                             \
+    rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG>(rg, lane_off, tap_base, spv, u0, vrow, p.w, rows_ok, \
+                                                            col_ok, nv, acc_max, acc_sum, xz_max, xz_sum, yzv)
+                if (AC == 16 && FORMULA == SSB_FORMULA_CANVAS && ((hdr >> 15) & 1u)) {
+                    // regular stage: taps at fixed box rows, one weight bracket (StageP)
+                    StageP spv = sm.sp[stage];
+                    spv.j0 += warp * ROWS;  // frame row of tap a of this warp's row 0
+                    const uint32_t tap_base = smem_addr(&sm.box[stage][0][0]) +
+                                              (uint32_t)(spv.a0 + warp * ROWS) * (2u * row_pitch<AC>()) + lane_off;
+                    if (fast) SSB_ROWS_PASS(true, true, true);
+                    else SSB_ROWS_PASS(false, true, true);
                 } else {
-                    if (chained)
-                        rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE, true, AC>(rg, lane_off, vrow, p.w, rows_ok,
-                                                                                 col_ok, nv, acc_max, acc_sum, xz_max,
-                                                                                 xz_sum, yzv);
-                    else
-                        rows_pass<INTERP, FORMULA, kMax, false, ROWS, SIDE, false, AC>(rg, lane_off, vrow, p.w, rows_ok,
-                                                                                  col_ok, nv, acc_max, acc_sum, xz_max,
-                                                                                  xz_sum, yzv);
+                    const StageP spv{};
+                    const uint32_t tap_base = 0;
+                    // four specialisations so the row loop has no per-row branches
+                    if (fast) {
+                        if (chained) SSB_ROWS_PASS(true, true, false);
+                        else SSB_ROWS_PASS(true, false, false);
+                    } else {
+                        if (chained) SSB_ROWS_PASS(false, true, false);
+                        else SSB_ROWS_PASS(false, false, false);
+                    }
                 }
+#undef SSB_ROWS_PASS
             } else if (vrow != nullptr && col_ok) {
                 const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -906,6 +975,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *reinterpret_cast<uint4 *>(dst) = xz_max;
                 } else {
                     uint32_t *dst = &sm.xz[(buf * kConsumerWarps + warp) * kTX + lane * 8];
+                    if (kBiased && live) {
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) xz_sum[c] -= (uint32_t)ROWS * kBias;
+                    }
                     *reinterpret_cast<uint4 *>(dst) = make_uint4(xz_sum[0], xz_sum[1], xz_sum[2], xz_sum[3]);
                     *reinterpret_cast<uint4 *>(dst + 4) = make_uint4(xz_sum[4], xz_sum[5], xz_sum[6], xz_sum[7]);
                 }
@@ -957,8 +1030,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        if (acc_sum[k][c] && (AC == 16 || c < nv)) red_u32<false>(dst + c, acc_sum[k][c]);
+                    for (int c = 0; c < 8; ++c) {
+                        const uint32_t v = acc_sum[k][c] - (kBiased ? n_live * kBias : 0u);
+                        if (v && (AC == 16 || c < nv)) red_u32<false>(dst + c, v);
+                    }
                 }
             }
         }
@@ -1023,7 +1098,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
 int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
     auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC>;
-    constexpr int smem = (int)sizeof(Smem<ROWS, AC>);
+    constexpr int smem = (int)sizeof(Smem<ROWS, AC, SIDE>);
+    static_assert(smem <= 227 * 1024, "shared memory budget");
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<grid, kThreads, smem, st>>>(map, prm);
     return check_launch("deskew_tma_kernel");

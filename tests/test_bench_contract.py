@@ -52,3 +52,27 @@ def test_reference_arm_is_bounded_for_many_steps():
     d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")][-1])
     assert d["steps"] == 40 and d["value"] > 0
     assert wall < 240, wall
+
+
+def test_reference_arm_config_matches_ours():
+    # same config keys as the GPU arm (the driver compares them field by field)
+    r = run(["--impl", "reference", "--config", "1", "--steps", "1", "--warmup", "1", "--ref-seconds", "1"])
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")][-1])
+    for k in ("workload", "interp", "shear_px", "canvas", "outputs"):
+        assert k in d["config"], k
+    # ms_per_step is one full stack's worth of reference work
+    n, (u, w) = 128, d["config"]["canvas"]
+    assert abs(d["ms_per_step"] - n * u * w / (d["value"] * 1e9) * 1e3) < 1e-6 * d["ms_per_step"]
+
+
+def test_gpus_n_self_launches_n_ranks_dry_run():
+    # `bench.py --gpus N` without torchrun re-executes itself with N ranks (gloo on CPU here)
+    for n in (2, 3):
+        r = run(["--gpus", str(n), "--dry-run", "--backend", "gloo", "--steps", "3", "--warmup", "3"])
+        assert r.returncode == 0, r.stderr[-2000:]
+        lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+        assert len(lines) == 1, r.stdout
+        d = json.loads(lines[0])
+        assert d["n_gpus"] == n and d["dry_run"] is True and d["value"] is None
+        assert d["config"]["workload"].startswith("config4") and d["config"]["display_gather_ok"] is True
+        assert d["config"]["stacks_per_rank"] == len(range(0, 64, n))
