@@ -109,7 +109,14 @@ struct alignas(16) RowP {
     uint32_t off_b;  // tap b (row j1)
     int32_t kind;    // npinterp only: 3 = dx == 1 (incl. copies, t = 0), 2 = general dx
     int32_t pad;
-    float w_lo, w_lo2, w_hi, w_hi2;  // fp32 bracket of the row weight, duplicated for f32x2 ops
+    union {
+        struct {
+            float w_lo, w_lo2, w_hi, w_hi2;  // fp32 bracket of the row weight, duplicated for f32x2 ops
+        };
+        struct {
+            double n0, n1;  // fp64 kernels (kF64): -c0 * 2^52, -c1 * 2^52
+        };
+    };
     double c0;       // canvas: w0 = 1-f       npinterp: t
     double c1;       // canvas: f              npinterp: dx
 };
@@ -326,6 +333,65 @@ __device__ __forceinline__ uint32_t lerp8_f32(const f32x2 (&A)[4], const f32x2 (
     return chk;
 }
 
+// ---- fp64 chained lerp (sum mode with XZ / YZ: a per-slice CTA barrier would make every stage wait
+// for the slowest warp's fp32-bracket fallback, so these kernels evaluate every voxel exactly in fp64)
+// Tap conversion for the chained canvas path (SSB_CVT_MODE):
+//   0  2^52 trick for every tap value: integer extract + constant high word, DFMA with -w*2^52;
+//   1  native I2F.F64 for every value (one conversion-pipe op, ~16/clk/SM on B200) + DMUL;
+//   2  mixed: low halves native (I2F.F64.U16 reads the half in place, no extract), high halves
+//      by the trick -- 1.5 issue slots per value and half the conversion-pipe load of mode 1.
+// All three give fl(w*a) exactly.  Measured on B200 (profiles/README.md): mode 2 is 2.6-3.4 %
+// faster than mode 0 projection-only and equal with a volume; mode 1 is slowest (conversion pipe).
+#ifndef SSB_CVT_MODE
+#define SSB_CVT_MODE 2
+#endif
+template <int C>
+__device__ __forceinline__ constexpr bool native_tap() {
+    return SSB_CVT_MODE == 1 || (SSB_CVT_MODE == 2 && (C & 1) == 0);
+}
+
+// I2F.F64.U16 of the low half of a 32-bit register (no separate extract)
+__device__ __forceinline__ double u16lo_to_f64(uint32_t w) {
+    double r;
+    asm("cvt.rn.f64.u16 %0, %1;" : "=d"(r) : "h"((unsigned short)w));
+    return r;
+}
+
+__device__ __forceinline__ void to_biased8(const uint4 t, double (&o)[8]) {
+    const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        o[2 * q] = (SSB_CVT_MODE != 0) ? u16lo_to_f64(w4[q]) : biased(w4[q] & 0xFFFFu);
+        o[2 * q + 1] = (SSB_CVT_MODE == 1) ? __uint2double_rn(w4[q] >> 16) : biased(w4[q] >> 16);
+    }
+}
+
+template <int C>
+__device__ __forceinline__ double tap_prod(double c, double a, double n) {
+    if (native_tap<C>()) return __dmul_rn(c, a);
+    return __fma_rn(c, a, n);
+}
+
+// canvas lerp of 8 voxels from converted taps: rint(fl(fl(w0*a) + fl(f*b))) as 8 u32 values
+template <int C>
+__device__ __forceinline__ uint32_t lerp_one(const double a, const double b, const double c0, const double c1,
+                                             const double n0, const double n1) {
+    return (uint32_t)__double2loint(__dadd_rn(__dadd_rn(tap_prod<C>(c0, a, n0), tap_prod<C>(c1, b, n1)), kRintMagic));
+}
+
+__device__ __forceinline__ void lerp_biased8_raw(const double (&a)[8], const double (&b)[8], const double c0,
+                                                 const double c1, const double n0, const double n1,
+                                                 uint32_t (&r)[8]) {
+    r[0] = lerp_one<0>(a[0], b[0], c0, c1, n0, n1);
+    r[1] = lerp_one<1>(a[1], b[1], c0, c1, n0, n1);
+    r[2] = lerp_one<2>(a[2], b[2], c0, c1, n0, n1);
+    r[3] = lerp_one<3>(a[3], b[3], c0, c1, n0, n1);
+    r[4] = lerp_one<4>(a[4], b[4], c0, c1, n0, n1);
+    r[5] = lerp_one<5>(a[5], b[5], c0, c1, n0, n1);
+    r[6] = lerp_one<6>(a[6], b[6], c0, c1, n0, n1);
+    r[7] = lerp_one<7>(a[7], b[7], c0, c1, n0, n1);
+}
+
 __device__ __forceinline__ uint4 pack8(const uint32_t (&r)[8]) {
     return make_uint4(__byte_perm(r[0], r[1], 0x5410), __byte_perm(r[2], r[3], 0x5410),
                       __byte_perm(r[4], r[5], 0x5410), __byte_perm(r[6], r[7], 0x5410));
@@ -448,7 +514,7 @@ __device__ __forceinline__ void set_bracket(RowP &o, double w) {
 // the row is live (inside the window and the slice's span).
 // Row-copy mode: frame row j of the slice sits at byte (d0 + 2*j*rs) & 15 of its slot (d0: the
 // alignment of row 0's first pixel of the tile); TMA mode: d0 = rs2 = 0.
-template <int INTERP, int FORMULA, int AC>
+template <int INTERP, int FORMULA, int AC, bool F64>
 __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int64_t lo, int64_t hi, double off,
                                          int64_t h, int64_t box_r0, int64_t box_rows, uint32_t box_addr,
                                          uint32_t zero_addr, uint32_t d0, uint32_t rs2) {
@@ -458,7 +524,12 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     o.kind = 3;
     o.pad = 0;
     if (FORMULA == SSB_FORMULA_NPINTERP) o.c0 = 0.0;  // t = 0: copy of tap a (the zero row)
-    set_bracket(o, 0.0);
+    if (F64) {
+        o.n0 = -(o.c0 * kTwo52);
+        o.n1 = -0.0;
+    } else {
+        set_bracket(o, 0.0);
+    }
     if (!in_window || u < lo || u > hi) return false;
     const RowParam rp = row_param<INTERP, FORMULA>(u, lo, off, h);
     // the box covers [box_r0, box_r0 + TU + 2*slack): a tap outside it would read another
@@ -472,7 +543,12 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
         o.c1 = rp.c1;
         o.kind = rp.kind;
         // weight of a + w*(b - a): canvas f; np.interp t (dx == 1) or t/dx
-        set_bracket(o, FORMULA == SSB_FORMULA_CANVAS ? rp.c1 : rp.kind == 3 ? rp.c0 : __ddiv_rn(rp.c0, rp.c1));
+        if (F64) {
+            o.n0 = -(rp.c0 * kTwo52);  // exact: power-of-two scaling
+            o.n1 = -(rp.c1 * kTwo52);
+        } else {
+            set_bracket(o, FORMULA == SSB_FORMULA_CANVAS ? rp.c1 : rp.kind == 3 ? rp.c0 : __ddiv_rn(rp.c0, rp.c1));
+        }
     } else if (FORMULA == SSB_FORMULA_CANVAS) {
         // copy (only reachable for h == 1 paths): w0 = 1, f = 0
         o.off_b = o.off_a;
@@ -543,8 +619,12 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         }
     };
     uint4 vs[kStream ? 1 : ROWS];
+    constexpr bool kF64 = !kMax && SIDE && INTERP == SSB_INTERP_LINEAR;  // see lerp_biased8_raw
+    constexpr bool chain32 = chain && !kF64, chain64 = chain && kF64 && FORMULA == SSB_FORMULA_CANVAS;
     f32x2 prev[4];
-    if (chain) to_f23(lds8<smem_ac<AC>()>(tap_a(0)), prev);
+    double prevd[8];
+    if (chain32) to_f23(lds8<smem_ac<AC>()>(tap_a(0)), prev);
+    if (chain64) to_biased8(lds8<smem_ac<AC>()>(tap_a(0)), prevd);
     f32x2 wlo_s = 0, whi_s = 0;
     if (REG) {
         wlo_s = f2pack(__float_as_uint(sp.w_lo), __float_as_uint(sp.w_lo));
@@ -555,12 +635,42 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         uint4 v;
         if (INTERP == SSB_INTERP_NEAREST) {
             v = lds8<smem_ac<AC>()>(tap_a(k));
+        } else if (kF64) {
+            // the producer writes full row tables for these kernels (no regular stages)
+            uint32_t bits[8];
+            const double c0 = rg[k].c0, c1 = rg[k].c1;
+            const int kind = rg[k].kind;
+            if (chain64) {
+                double cur[8];
+                to_biased8(lds8<smem_ac<AC>()>(tap_b(k)), cur);
+                uint32_t r[8];
+                lerp_biased8_raw(prevd, cur, c0, c1, rg[k].n0, rg[k].n1, bits);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) prevd[c] = cur[c];
+            } else {
+                exact8<FORMULA>(lds8<smem_ac<AC>()>(tap_a(k)), lds8<smem_ac<AC>()>(tap_b(k)), c0, c1, kind, bits);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) bits[c] &= 0xFFFFu;  // unbiased: these kernels sum plain voxels
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (kEdge && c >= nv) bits[c] = 0u;
+            put(k, pack8(bits));
+            uint32_t rs = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                acc_sum[k][c] += bits[c];
+                xz_sum[c] += bits[c];
+                rs += bits[c];
+            }
+            yzv[k] = redux_add(rs);
+            continue;
         } else {
             // fp32 bracket of the lerp (RowP); chained taps: tap row k+1 is tap b of row k and
             // tap a of row k+1, converted once
             f32x2 A[4], B[4];
             to_f23(lds8<smem_ac<AC>()>(tap_b(k)), B);
-            if (chain) {
+            if (chain32) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) A[q] = prev[q];
             } else {
@@ -583,7 +693,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                     exact8<FORMULA>(ta, tb, rg[k].c0, rg[k].c1, rg[k].kind, bits);
                 }
             }
-            if (chain) {
+            if (chain32) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) prev[q] = B[q];
             }
@@ -626,6 +736,8 @@ template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
 __global__ void __launch_bounds__(kThreads, 1)
     deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
+    // sum mode with XZ / YZ evaluates voxels in fp64 (see lerp_biased8_raw) from full row tables
+    constexpr bool kF64 = !kMax && SIDE && INTERP == SSB_INTERP_LINEAR;
     using C = Cfg<ROWS, SIDE>;
     constexpr int kTU = C::kTU;
     constexpr int kStages = C::kStages;
@@ -773,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // frac(off) away from 0 and 1 by 2^-30, |u - off| < 2^20): taps j0 + r, j0 + r + 1
                 // unclamped and f = 1 - phi within (H + 2) * 2^-52
                 bool regular = false;
-                if (AC == 16 && FORMULA == SSB_FORMULA_CANVAS && hit && SSB_REGULAR_STAGES &&
+                if (AC == 16 && FORMULA == SSB_FORMULA_CANVAS && hit && SSB_REGULAR_STAGES && !kF64 &&
                     (int64_t)(ut + 1) * kTU <= p.u_count && lo <= tu0 && tu0 + kTU - 1 <= hi && p.h < (1 << 20)) {
                     StageP spv;
                     spv.off = off;
@@ -812,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int r = lane + 32 * j;
                         bool l = false;
                         if (r < kTU)
-                            l = make_row<INTERP, FORMULA, AC>(sm.rows[stage][r], tu0 + r,
+                            l = make_row<INTERP, FORMULA, AC, kF64>(sm.rows[stage][r], tu0 + r,
                                                               (int64_t)ut * kTU + r < p.u_count, lo, hi, off, p.h,
                                                               box_r0, C::template box_rows<INTERP, FORMULA>(),
                                                               box_addr, zero_addr, d0, rs2);
@@ -892,7 +1004,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         const int ns = (int)(s_end - s_begin);
         // linear sums carry 2^23-biased voxels (rows_pass): bias to remove per live pass
-        constexpr bool kBiased = !kMax && INTERP == SSB_INTERP_LINEAR;
+        constexpr bool kBiased = !kMax && INTERP == SSB_INTERP_LINEAR && !kF64;
         uint32_t n_live = 0;
         for (int si = 0; si < ns; ++si) {
             mbar_wait(&sm.full[stage], sphase);
@@ -911,7 +1023,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define SSB_ROWS_PASS(F, CH, RG)                                                                             \
     rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG>(rg, lane_off, tap_base, spv, u0, vrow, p.w, rows_ok, \
                                                             col_ok, nv, acc_max, acc_sum, xz_max, xz_sum, yzv)
-                if (AC == 16 && FORMULA == SSB_FORMULA_CANVAS && ((hdr >> 15) & 1u)) {
+                if (AC == 16 && FORMULA == SSB_FORMULA_CANVAS && !kF64 && ((hdr >> 15) & 1u)) {
                     // regular stage: taps at fixed box rows, one weight bracket (StageP)
                     StageP spv = sm.sp[stage];
                     spv.j0 += warp * ROWS;  // frame row of tap a of this warp's row 0
