@@ -262,6 +262,8 @@ extern "C" int ssb_rolling_band(const uint16_t *ring, const uint8_t *present, in
                                 int64_t canvas_rows, int64_t replaced, void *workspace, size_t workspace_bytes,
                                 void *stream) {
     if (n_ring < 1 || height < 1 || width < 1) return fail(SSB_ERR_PARAM, "bad ring shape");
+    if (ring == nullptr || present == nullptr || canvas == nullptr || contributor == nullptr)
+        return fail(SSB_ERR_PARAM, "ring, present, canvas and contributor must be device buffers");
     if (!(shear_px >= 0.0)) return fail(SSB_ERR_PARAM, "shear_px must be >= 0");
     if (interp != SSB_INTERP_NEAREST && interp != SSB_INTERP_LINEAR)
         return fail(SSB_ERR_PARAM, "interp must be nearest or linear");

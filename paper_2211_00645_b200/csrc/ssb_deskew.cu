@@ -371,9 +371,12 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (d->n == 0 || d->u_count == 0) {
         // nothing placed: projections of an empty window are zero (XY unless accumulating)
+        // (and XZ (n, W) / YZ (n, u_count) of an empty window: all-zero rows)
         const size_t esz = d->reduce == SSB_REDUCE_MAX ? 2 : 4;
         if (xy && !(d->flags & SSB_FLAG_XY_ACCUMULATE))
             cudaMemsetAsync(xy, 0, (size_t)d->u_count * d->width * esz, st);
+        if (xz) cudaMemsetAsync(xz, 0, (size_t)d->n * d->width * esz, st);
+        if (yz) cudaMemsetAsync(yz, 0, (size_t)d->n * d->u_count * esz, st);
         return check_launch("ssb_deskew(empty)");
     }
     if (raw == nullptr) return fail(SSB_ERR_PARAM, "raw frames pointer is null");

@@ -34,17 +34,11 @@ PIXEL_FORMATS = {"gray16": 0, "gray8": 1}
 MODES = {"global": 0, "rolling": 1}
 _MAX_DIM = 2**31 - 1
 
-_stats_cache: dict = {}
-
-
 def _stats_buffer(device: torch.device) -> torch.Tensor:
-    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
-    buf = _stats_cache.get(key)
-    if buf is None:
-        nbytes = int(_lib.load().ssb_encode_gray8_stats_bytes())
-        buf = torch.empty(nbytes // 4, dtype=torch.int32, device=device)
-        _stats_cache[key] = buf
-    return buf
+    """A fresh result buffer per call (caching allocator, on the current stream): a later encode on
+    the same stream cannot overwrite the (g8_offset, g8_range) a caller has not read yet."""
+    nbytes = int(_lib.load().ssb_encode_gray8_stats_bytes())
+    return torch.empty(nbytes // 4, dtype=torch.int32, device=device)
 
 
 def _as_device_u16(pixels) -> torch.Tensor:
@@ -68,11 +62,18 @@ def encode_gray8_device(pixels, stream: torch.cuda.Stream | None = None):
     ``stream`` (default: the current stream).  An empty image raises ValueError, as numpy's
     ``min()`` does in the reference.
     """
-    t = _as_device_u16(pixels)
+    dev = pixels.device if isinstance(pixels, torch.Tensor) and pixels.is_cuda else require_cuda()
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    producer = torch.cuda.current_stream(dev)
+    if st != producer:
+        st.wait_stream(producer)  # a device image written on the caller's stream is complete
+    with torch.cuda.stream(st):  # upload / contiguous copy ordered before the kernel on `st`
+        t = _as_device_u16(pixels)
     if t.numel() == 0:
         raise ValueError("zero-size array to reduction operation minimum which has no identity")
+    if st != producer and isinstance(pixels, torch.Tensor) and pixels.is_cuda:
+        t.record_stream(st)  # the caller's tensor may be freed while `st` still reads it
     lib = _lib.load()
-    st = stream if stream is not None else torch.cuda.current_stream(t.device)
     with torch.cuda.stream(st):
         stats = _stats_buffer(t.device)
         out = torch.empty(t.shape, dtype=torch.uint8, device=t.device)

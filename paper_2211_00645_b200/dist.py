@@ -119,6 +119,7 @@ def _narrow(t: torch.Tensor, reduce: str) -> torch.Tensor:
 
 def combine_xy(partial: torch.Tensor, plan: SlabPlan, width: int, reduce: str = "sum", dst: int = 0,
                group=None):
+    # ``dst`` is a global rank (torch.distributed's convention for reduce / gather with a group)
     """Merge per-slab XY windows into the full (U, W) canvas on rank ``dst``.
 
     Every rank places its window into a zeroed full canvas and one NCCL reduce
@@ -131,7 +132,7 @@ def combine_xy(partial: torch.Tensor, plan: SlabPlan, width: int, reduce: str = 
         full[plan.u_begin:plan.u_begin + plan.u_count] = _wide(partial, reduce)
     op = dist.ReduceOp.MAX if reduce == "max" else dist.ReduceOp.SUM
     dist.reduce(full, dst=dst, op=op, group=group)
-    if dist.get_rank(group) != dst:
+    if dist.get_rank() != dst:
         return None
     return _narrow(full, reduce)
 
@@ -151,7 +152,7 @@ def gather_slices(partial: torch.Tensor, plans: list, rank: int, length: int, re
             buf[:plan.count, plan.u_begin:plan.u_begin + plan.u_count] = _wide(partial, reduce)
         else:
             buf[:plan.count] = _wide(partial, reduce)
-    bufs = [torch.empty_like(buf) for _ in plans] if dist.get_rank(group) == dst else None
+    bufs = [torch.empty_like(buf) for _ in plans] if dist.get_rank() == dst else None
     dist.gather(buf, bufs, dst=dst, group=group)
     if bufs is None:
         return None
@@ -167,6 +168,6 @@ def gather_to_display(projection: torch.Tensor, dst: int = 0, group=None):
     """
     t = projection.contiguous().view(torch.uint8)
     world = dist.get_world_size(group)
-    bufs = [torch.empty_like(t) for _ in range(world)] if dist.get_rank(group) == dst else None
+    bufs = [torch.empty_like(t) for _ in range(world)] if dist.get_rank() == dst else None
     dist.gather(t, bufs, dst=dst, group=group)
     return None if bufs is None else [b.view(torch.uint16) for b in bufs]

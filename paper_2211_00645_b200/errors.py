@@ -7,7 +7,12 @@ keep working. C-ABI status codes (``include/ssb.h``) map onto these in
 """
 
 
-class SkewstreamError(Exception):
+class _Root(Exception):
+    """Heap-type base, so ``adopt`` can rebase SkewstreamError (a class whose only base is the builtin
+    Exception cannot take a Python-defined base: CPython checks the instance layout)."""
+
+
+class SkewstreamError(_Root):
     """Root of every error raised by this package (ss/errors.py:4)."""
 
 
@@ -33,3 +38,22 @@ class EndOfStream(SkewstreamError):
 
 class DeviceError(SkewstreamError):
     """A CUDA call failed, or the native library is missing on a GPU box."""
+
+
+_CLASSES = ("SkewstreamError", "ParameterError", "CapacityError", "ProtocolError", "MetadataError", "EndOfStream")
+
+
+def adopt(ref_errors) -> None:
+    """Make each class above a subclass of the same-named class of another errors module.
+
+    The switch-over shim inside ``skewstream`` calls ``adopt(skewstream.errors)``
+    once, so code that catches the reference's exceptions (``except skewstream.errors.ParameterError``,
+    ``pytest.raises(CapacityError)``) also catches the drop-in's.  Idempotent; the root goes first so
+    every rebased class keeps a consistent method resolution order.
+    """
+    g = globals()
+    for name in _CLASSES:
+        ours, theirs = g[name], getattr(ref_errors, name, None)
+        if theirs is None or theirs is ours or issubclass(ours, theirs):
+            continue
+        ours.__bases__ = (theirs,) + ours.__bases__

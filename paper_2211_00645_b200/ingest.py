@@ -100,15 +100,14 @@ def _read_parallel(path, view: memoryview, size: int, threads: int = 8, piece: i
 def _load_raw(path, geom: SheetGeometry, count, pinned: bool, out=None) -> np.ndarray:
     w, h = geom.frame_width_px, geom.frame_height_px
     frame_px = w * h
-    size = os.path.getsize(path)
-    px = size // 2
-    if size % 2 or px == 0 or px % frame_px != 0:
+    px = os.path.getsize(path) // 2  # np.fromfile ignores a trailing odd byte (ss/source.py:434)
+    if px == 0 or px % frame_px != 0:
         raise MetadataError(f"raw file holds {px} pixels, not a multiple of the sidecar frame size {w}x{h}")
     n = px // frame_px
     if count is not None and n != count:
         raise MetadataError(f"raw file holds {n} frames, sidecar says {count}")
     out = _alloc(n, h, w, pinned, out)
-    _read_parallel(path, memoryview(out.reshape(-1).view(np.uint8)), size)
+    _read_parallel(path, memoryview(out.reshape(-1).view(np.uint8)), 2 * px)
     if sys.byteorder == "big":  # the file is little-endian ("<u2", ss/source.py:384)
         out.byteswap(inplace=True)
     return out
@@ -118,10 +117,13 @@ def _load_tiff(path, geom: SheetGeometry, count, pinned: bool, out=None) -> np.n
     from PIL import Image
 
     w, h = geom.frame_width_px, geom.frame_height_px
+    # the reference's order of faults (ss/source.py:448-474): any page's pixel type while reading,
+    # then page shapes, then the page count
+    shape_fault = None
     try:
         with Image.open(path) as im:
             n = getattr(im, "n_frames", 1)
-            if count is not None and n != count:
+            if out is not None and count is not None and n != count:  # a caller buffer sized by the sidecar
                 raise MetadataError(f"TIFF holds {n} pages, sidecar says {count}")
             out = _alloc(n, h, w, pinned, out)
             for i in range(n):
@@ -130,10 +132,16 @@ def _load_tiff(path, geom: SheetGeometry, count, pinned: bool, out=None) -> np.n
                 if arr.dtype.itemsize != 2 or arr.ndim != 2:
                     raise MetadataError(f"page {i} is not 16-bit grayscale ({arr.dtype}, {arr.ndim}-D)")
                 if arr.shape != (h, w):
-                    raise MetadataError(f"TIFF page {i} is {arr.shape[1]}x{arr.shape[0]}, sidecar says {w}x{h}")
+                    if shape_fault is None:
+                        shape_fault = f"TIFF page {i} is {arr.shape[1]}x{arr.shape[0]}, sidecar says {w}x{h}"
+                    continue
                 out[i] = arr
     except (OSError, SyntaxError) as exc:
         raise MetadataError(f"cannot read TIFF {path}: {exc}") from exc
+    if shape_fault is not None:
+        raise MetadataError(shape_fault)
+    if count is not None and n != count:
+        raise MetadataError(f"TIFF holds {n} pages, sidecar says {count}")
     return out
 
 

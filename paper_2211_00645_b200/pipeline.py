@@ -110,6 +110,44 @@ def _vp(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+class _HostView(np.ndarray):
+    """Host copy of a device canvas buffer (``max_pixels`` / ``contributor``).
+
+    The reference's canvas buffers are plain mutable arrays (ss/pipeline.py:267-270).  Writes into
+    this copy or any view of it -- item assignment or a ufunc with ``out=`` -- mark the owning
+    canvas dirty, and its next device operation uploads the host copy first, so an in-place caller
+    write is never dropped.  Copies (``.copy()``, ``np.array``) are independent, as in numpy.
+    """
+
+    def __array_finalize__(self, obj):
+        # views share the owner; fresh arrays (copies) do not
+        self._owner = getattr(obj, "_owner", None) if self.base is not None else None
+
+    def _touch(self):
+        if self._owner is not None:
+            self._owner._host_dirty = True
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        self._touch()
+
+    def __array_ufunc__(self, ufunc, method, *inputs, out=None, **kwargs):
+        args = [x.view(np.ndarray) if isinstance(x, _HostView) else x for x in inputs]
+        if out is not None:
+            kwargs["out"] = tuple(o.view(np.ndarray) if isinstance(o, _HostView) else o for o in out)
+        res = getattr(ufunc, method)(*args, **kwargs)
+        for o in out or ():
+            if isinstance(o, _HostView):
+                o._touch()
+        return res
+
+
+def _host_view(t: torch.Tensor, owner) -> "_HostView":
+    v = t.cpu().numpy().view(_HostView)
+    v._owner = owner
+    return v
+
+
 class ProjectionCanvas:
     """Enlarged max-projection canvas of one channel, resident in HBM.
 
@@ -140,6 +178,7 @@ class ProjectionCanvas:
         self._present_dev = None   # (N,) uint8
         self._roll_ws = None       # device list of voxels to re-max (incremental rolling updates)
         self._host_cache = None
+        self._host_dirty = False
         self._pending_uploads: list = []  # (copy-done event, pinned host buffer) still being read
         self._staging = None              # pinned two-slot ring for pageable frames: (buffer, event)
         self._stage_next = 0
@@ -209,17 +248,31 @@ class ProjectionCanvas:
 
     @property
     def max_pixels(self) -> np.ndarray:
-        """Host copy of the canvas (ss/pipeline.py:267)."""
+        """Host copy of the canvas (ss/pipeline.py:267); in-place writes reach the device canvas
+        before its next operation (``_HostView``)."""
         if self._host_cache is None:
             self.stream.synchronize()
-            self._host_cache = (self.max_pixels_device.cpu().numpy(),
-                                self.contributor_device.cpu().numpy())
+            self._host_cache = (_host_view(self.max_pixels_device, self), _host_view(self.contributor_device, self))
+            self._host_dirty = False
         return self._host_cache[0]
+
+    def _flush_host_writes(self) -> None:
+        """Upload host copies that a caller wrote into (see ``_HostView``) before a device op."""
+        if not self._host_dirty or self._host_cache is None:
+            return
+        mp, ct = self._host_cache
+        with torch.cuda.stream(self.stream):
+            self.max_pixels_device.copy_(torch.from_numpy(np.ascontiguousarray(mp.view(np.ndarray))))
+            self.contributor_device.copy_(torch.from_numpy(np.ascontiguousarray(ct.view(np.ndarray))))
+        self.stream.synchronize()  # the host arrays may be written again right away
+        self._host_dirty = False
+        self._exact = self._canvas_zero = False
 
     @max_pixels.setter
     def max_pixels(self, value) -> None:
         arr = np.ascontiguousarray(value, dtype=np.uint16)
         self.height, self.width = arr.shape
+        self._flush_host_writes()  # the other buffer's pending host writes
         with torch.cuda.stream(self.stream):
             self.max_pixels_device = torch.from_numpy(arr).to(self._device)
         self._host_cache = None
@@ -234,6 +287,7 @@ class ProjectionCanvas:
     @contributor.setter
     def contributor(self, value) -> None:
         arr = np.ascontiguousarray(value, dtype=np.int16)
+        self._flush_host_writes()
         with torch.cuda.stream(self.stream):
             self.contributor_device = torch.from_numpy(arr).to(self._device)
         self._host_cache = None
@@ -251,9 +305,11 @@ class ProjectionCanvas:
         if self._present_dev is not None:
             with torch.cuda.stream(self.stream):
                 self._present_dev.zero_()
-            for k, rf in enumerate(self._ring):
-                if rf is not None:
-                    self._ring_store(rf)
+        # the device ring mirrors the assigned frames (allocated by the first store), so a rolling
+        # replace_all right after the assignment re-maxes from resident frames
+        for rf in self._ring:
+            if rf is not None:
+                self._ring_store(rf)
 
     # -- placement grid --------------------------------------------------------
     def row_span(self, slice_index: int) -> tuple[int, int]:
@@ -280,6 +336,7 @@ class ProjectionCanvas:
     def place(self, frame: RawFrame) -> tuple[int, int]:
         """Max-accumulate one slice into the device canvas (ss/pipeline.py:316-323)."""
         self._check_frame(frame)
+        self._flush_host_writes()
         lo, hi = self.row_span(frame.slice_index)
         raw = self._upload(frame.pixels)
         # one fused launch over the slice's band: rows lo..hi, XY folded in place
@@ -295,6 +352,7 @@ class ProjectionCanvas:
 
     def place_stack(self, frames: torch.Tensor, first_slice: int = 0) -> None:
         """Place n consecutive device-resident slices in one fused launch."""
+        self._flush_host_writes()
         n = int(frames.shape[0])
         if first_slice < 0 or first_slice + n > self.geom.slice_count:
             raise ParameterError("slice range out of range")
@@ -321,6 +379,7 @@ class ProjectionCanvas:
 
     def finalize_global_device(self) -> torch.Tensor:
         """Device variant: returns a device copy without a host sync."""
+        self._flush_host_writes()
         if not all(self._placed):
             raise ProtocolError(f"finalize with {self._placed.count(False)} slice(s) not yet placed")
         with torch.cuda.stream(self.stream):
@@ -329,6 +388,7 @@ class ProjectionCanvas:
         return out
 
     def reset(self) -> None:
+        self._flush_host_writes()
         with torch.cuda.stream(self.stream):
             self.max_pixels_device.zero_()
             self.contributor_device.fill_(-1)
@@ -353,6 +413,7 @@ class ProjectionCanvas:
 
     def rolling_replace(self, frame: RawFrame) -> tuple[int, int]:
         """Swap in the newest version of a slice and refresh its band (ss/pipeline.py:345-359)."""
+        self._flush_host_writes()
         if self.mode != "rolling":
             raise ProtocolError("rolling_replace on a canvas in global mode")
         self._check_frame(frame)
@@ -369,6 +430,11 @@ class ProjectionCanvas:
         full ring re-max (``_exact``); otherwise the whole band is re-maxed.
         """
         lib = _lib.load()
+        if self._ring_dev is None:  # nothing stored yet: an all-absent ring of the right shape
+            with torch.cuda.stream(self.stream):
+                self._ring_dev = torch.zeros((self.geom.slice_count, self.geom.frame_height_px, self.width),
+                                             dtype=torch.uint16, device=self._device)
+                self._present_dev = torch.zeros((self.geom.slice_count,), dtype=torch.uint8, device=self._device)
         ws, ws_bytes = None, 0
         if replaced >= 0:
             ws_bytes = int(lib.ssb_rolling_workspace_bytes(hi - lo + 1, self.width))

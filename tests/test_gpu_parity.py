@@ -657,3 +657,23 @@ def test_deskew_graph_replay_matches_direct_calls():
             np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
         st = rng.integers(0, 65536, st.shape).astype(np.uint16)
         raw.copy_(torch.from_numpy(st))
+
+
+def test_canvas_host_writes_reach_device():
+    """In-place writes into ProjectionCanvas.max_pixels (a mutable array in the reference,
+    ss/pipeline.py:267) are uploaded before the next device operation, not dropped."""
+    from paper_2211_00645_b200.geometry import SheetGeometry
+    from paper_2211_00645_b200.pipeline import ProjectionCanvas, RawFrame
+
+    g = SheetGeometry(alpha_deg=30.0, scan_step_um=0.115, pixel_pitch_um=0.115, slice_count=3,
+                      frame_width_px=8, frame_height_px=4)
+    c = ProjectionCanvas(g, 1.0, interp="nearest")
+    c.max_pixels[0, :] = 500  # caller write into the host copy
+    c.place(RawFrame(pixels=np.full((4, 8), 7, dtype=np.uint16), slice_index=1))
+    got = c.max_pixels
+    assert (got[0] == 500).all() and (got[1:5] == 7).all()
+    np.maximum(c.max_pixels[5:6], 9, out=c.max_pixels[5:6])  # ufunc out= into a view
+    for i in (0, 2):
+        c.place(RawFrame(pixels=np.zeros((4, 8), dtype=np.uint16), slice_index=i))
+    out = c.finalize_global()
+    assert (out[0] == 500).all() and (out[5] == 9).all() and (out[1:5] == 7).all()

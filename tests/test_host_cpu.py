@@ -161,3 +161,63 @@ class TestWorkspaceCache:
             assert ws.get(10, FakeStream(0)) is not bufs[0]  # evicted entry re-created
         finally:
             torch.cuda.stream = orig
+
+
+class TestHostView:
+    """ProjectionCanvas.max_pixels / contributor host copies (pipeline._HostView): in-place writes
+    mark the canvas dirty so the device copy is refreshed before its next operation."""
+
+    class Owner:
+        _host_dirty = False
+
+    def make(self):
+        from paper_2211_00645_b200.pipeline import _HostView
+
+        o = self.Owner()
+        v = np.zeros((4, 3), dtype=np.uint16).view(_HostView)
+        v._owner = o
+        return o, v
+
+    def test_item_and_view_writes_mark_dirty(self):
+        o, v = self.make()
+        _ = v[1:3].sum(), v.max()  # reads do not
+        assert not o._host_dirty
+        v[1, 2] = 7
+        assert o._host_dirty and v[1, 2] == 7
+        o._host_dirty = False
+        v[2:][0, 0] = 3  # through a view
+        assert o._host_dirty
+
+    def test_ufunc_out_marks_dirty_but_copies_do_not(self):
+        o, v = self.make()
+        np.maximum(v[0:2], 9, out=v[0:2])  # the reference's place() idiom (ss/pipeline.py:321)
+        assert o._host_dirty and int(v[:2].min()) == 9
+        o._host_dirty = False
+        c = v.copy()
+        c[0, 0] = 1
+        a = np.array(v)
+        a[0, 0] = 2
+        assert not o._host_dirty and v[0, 0] == 9
+
+
+def test_errors_adopt_reference_classes():
+    """errors.adopt(skewstream.errors): the reference's except clauses catch the drop-in's errors."""
+    import os
+    import sys
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "skewstream")):
+        pytest.skip("reference not installed (baseline/install_ref.sh)")
+    sys.path.insert(0, ref)
+    import skewstream.errors as R
+
+    from paper_2211_00645_b200 import errors as E
+
+    E.adopt(R)
+    E.adopt(R)  # idempotent
+    for name in E._CLASSES:
+        assert issubclass(getattr(E, name), getattr(R, name)), name
+    assert issubclass(E.ParameterError, ValueError)
+    assert issubclass(E.DeviceError, R.SkewstreamError)
+    with pytest.raises(R.CapacityError):
+        raise E.CapacityError("span outside canvas")
