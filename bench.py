@@ -420,6 +420,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             gt = sorted(a0.elapsed_time(a1) for a0, a1 in pairs)
             batch["cuda_graph_step_ms"] = gt[len(gt) // 2]
             del dg
+    batched = None
+    if flush is not None and world == 1 and args.batch > 1:
+        batched = run_batched(args, raw, s, interp, reduce, n, h, w, u, dev, stream)
     del flush
     clk = clocks.stop()
     if world > 1:
@@ -520,7 +523,51 @@ def run_ours(args, cfg, rank, world, local_rank):
         }
         if batch is not None:
             line["reference_deskew_gpu"] = batch
+        if batched is not None:
+            line["batched"] = batched
         print(json.dumps(line), flush=True)
+
+
+def run_batched(args, raw, s, interp, reduce, n, h, w, u, dev, stream):
+    """Small stacks (config 1): B distinct stacks deskewed by one persistent launch
+    (deskew.deskew_batch -> ssb_deskew_batch), volume + 3 MIPs each.  B stacks (1.3 GB at B = 16)
+    exceed the L2, so no flush; the main kernel is timed per launch inside libssb."""
+    import torch
+
+    from paper_2211_00645_b200 import _lib
+    from paper_2211_00645_b200.deskew import deskew_batch
+
+    B = args.batch
+    stacks = torch.empty((B, n, h, w), dtype=torch.uint16, device=dev)
+    for k in range(B):  # the config-4 rule: stack k = (stack 0 + 37 k) mod 4096
+        stacks[k] = ((raw.to(torch.int32) + 37 * k) % 4096).to(torch.uint16)
+    res = deskew_batch(stacks, s, interp, reduce=reduce, stream=stream)
+    for _ in range(max(3, args.warmup)):
+        deskew_batch(stacks, s, interp, reduce=reduce, volume=res.volume, projections=res.projections, stream=stream)
+    torch.cuda.synchronize()
+    _lib.profile_enable(True)
+    _lib.profile_read()
+    k = max(5, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        deskew_batch(stacks, s, interp, reduce=reduce, volume=res.volume, projections=res.projections, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    _lib.profile_enable(False)
+    kern_ms, kern_n = _lib.profile_read()
+    ms = e0.elapsed_time(e1) / k
+    kern = kern_ms / max(kern_n, 1)
+    nbytes = B * algorithmic_bytes(n, h, w, u, True, (0, 1, 2), reduce)
+    peak, peak_kind = peaks()
+    return {"stacks_per_launch": B, "ms_per_launch": ms, "value": B * n * u * w / (ms * 1e-3) / 1e9,
+            "unit": "GVoxels/s", "stacks_per_s": B * 1e3 / ms, "ms_per_stack": ms / B,
+            "roofline": {"bound": "hbm", "achieved": nbytes / (kern * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": nbytes / (kern * 1e-3) / 1e9 / peak, "peak_kind": peak_kind,
+                         "bytes_per_launch": nbytes, "kernel_ms": kern,
+                         "traffic": lookup_traffic(n, h, w, interp, f"batch{B}/volume+xy,xz,yz", reduce)},
+            "what": "deskew.deskew_batch: B distinct stacks (B x 82 MB > L2, no flush), one persistent launch "
+                    "(ssb_deskew_batch) + finalize per step"}
 
 
 def run_stream(args, cfg, rank, world, local_rank):
@@ -732,6 +779,7 @@ def main():
                     help="N > 1: gather each step's XY before the next deskew instead of overlapping")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunk-frames", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=16, help="config 1: stacks per batched launch (0/1: off)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--dry-run", action="store_true", help="N-rank launch/gather/timing plumbing only (no kernels)")
     args = ap.parse_args()

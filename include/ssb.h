@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SSB_VERSION 100
+#define SSB_VERSION 200
 
 /* status codes; Python maps them onto ss/errors.py classes */
 #define SSB_OK 0
@@ -99,6 +99,20 @@ size_t ssb_deskew_workspace_bytes(const ssb_deskew_desc *d);
  */
 int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz,
                void *yz, void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Batched fused deskew: `batch` stacks of one shape in one persistent launch.  Small stacks
+ * (BASELINE config 1: 128 x 256 x 512) leave most of the 148 SMs idle one launch at a time; the
+ * reference deskews them one canvas after another (ss/cli.py:332-338).  raw: device
+ * (batch, n, H, W) uint16, stacks back to back (stack stride = n * frame stride of the descriptor);
+ * vol (batch, n, U, W) or NULL; xy (batch, U, W), xz (batch, n, W), yz (batch, n, U), uint16 (max) or
+ * uint32 (sum), each may be NULL.  Stack b's outputs equal ssb_deskew on stack b alone (falls back to
+ * one launch per stack where the frames cannot take TMA boxes).  workspace:
+ * >= ssb_deskew_batch_workspace_bytes(d, batch).
+ */
+size_t ssb_deskew_batch_workspace_bytes(const ssb_deskew_desc *d, int64_t batch);
+int ssb_deskew_batch(const ssb_deskew_desc *d, int64_t batch, const uint16_t *raw, uint16_t *vol, void *xy,
+                     void *xz, void *yz, void *workspace, size_t workspace_bytes, void *stream);
 
 /*
  * Rolling-mode band recompute.  Replaces ProjectionCanvas._recompute_band

@@ -26,7 +26,7 @@ FLAG_XY_ACCUMULATE = 1
 #: every symbol include/ssb.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ssb_version", "ssb_last_error", "ssb_launch_count", "ssb_profile_enable",
            "ssb_profile_read", "ssb_deskew_workspace_bytes",
-           "ssb_deskew", "ssb_rolling_workspace_bytes", "ssb_rolling_band", "ssb_warp_rows", "ssb_combine",
+           "ssb_deskew", "ssb_deskew_batch_workspace_bytes", "ssb_deskew_batch", "ssb_rolling_workspace_bytes", "ssb_rolling_band", "ssb_warp_rows", "ssb_combine",
            "ssb_encode_gray8_stats_bytes", "ssb_encode_gray8")
 
 
@@ -79,6 +79,10 @@ def load(path: str = LIB_PATH):
         lib.ssb_deskew_workspace_bytes.restype = ctypes.c_size_t
         lib.ssb_deskew.argtypes = [pdesc, p, p, p, p, p, p, ctypes.c_size_t, p]
         lib.ssb_deskew.restype = ctypes.c_int
+        lib.ssb_deskew_batch_workspace_bytes.argtypes = [pdesc, i64]
+        lib.ssb_deskew_batch_workspace_bytes.restype = ctypes.c_size_t
+        lib.ssb_deskew_batch.argtypes = [pdesc, i64, p, p, p, p, p, p, ctypes.c_size_t, p]
+        lib.ssb_deskew_batch.restype = ctypes.c_int
         lib.ssb_rolling_workspace_bytes.argtypes = [i64, i64]
         lib.ssb_rolling_workspace_bytes.restype = ctypes.c_size_t
         lib.ssb_rolling_band.argtypes = [p, p, i64, i64, i64, d, i32, i64, i64, p, p, i64, i64, p, ctypes.c_size_t, p]

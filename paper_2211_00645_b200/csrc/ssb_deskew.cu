@@ -443,3 +443,35 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
     if (pl.yz_ws) launch_reduce(yz_dst, yz, pl.XT, d->n * d->u_count, is_max, false, st);
     return check_launch("reduce_planes_kernel");
 }
+
+extern "C" size_t ssb_deskew_batch_workspace_bytes(const ssb_deskew_desc *d, int64_t batch) {
+    if (validate(d) != SSB_OK || batch < 1) return 0;
+    return std::max(ssb_deskew_workspace_bytes(d), tma_workspace_bytes(*d, batch));
+}
+
+extern "C" int ssb_deskew_batch(const ssb_deskew_desc *d, int64_t batch, const uint16_t *raw, uint16_t *vol,
+                                void *xy, void *xz, void *yz, void *workspace, size_t workspace_bytes,
+                                void *stream) {
+    if (int rc = validate(d)) return rc;
+    if (batch < 1) return fail(SSB_ERR_PARAM, "batch must be >= 1, got %lld", (long long)batch);
+    if (batch == 1) return ssb_deskew(d, raw, vol, xy, xz, yz, workspace, workspace_bytes, stream);
+    if (raw == nullptr && d->n > 0) return fail(SSB_ERR_PARAM, "raw frames pointer is null");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t fs = frame_stride_of(*d);
+    // one persistent launch over every stack when the frames reach shared memory by TMA boxes
+    // (stacks back to back: stack b's frame k is frame b*n + k of one tensor map)
+    if (d->n > 0 && d->u_count > 0 && env_int("SSB_DISABLE_TMA", 0) == 0 &&
+        persistent_access_class(*d, raw, vol, xy) == 16)
+        return launch_deskew_tma(*d, raw, vol, xy, xz, yz, workspace, workspace_bytes, st, 16, batch);
+    // otherwise stack by stack (same results, one launch each)
+    const size_t esz = d->reduce == SSB_REDUCE_MAX ? 2 : 4;
+    for (int64_t b = 0; b < batch; ++b) {
+        const int rc = ssb_deskew(
+            d, raw ? raw + b * d->n * fs : nullptr, vol ? vol + b * d->n * d->u_count * d->width : nullptr,
+            xy ? static_cast<char *>(xy) + b * d->u_count * d->width * esz : nullptr,
+            xz ? static_cast<char *>(xz) + b * d->n * d->width * esz : nullptr,
+            yz ? static_cast<char *>(yz) + b * d->n * d->u_count * esz : nullptr, workspace, workspace_bytes, stream);
+        if (rc) return rc;
+    }
+    return SSB_OK;
+}

@@ -146,6 +146,10 @@ struct Params {
     int32_t big_pct;     // (clip) phase-1 share of a tile's slice range, percent
     const uint16_t *raw;  // row-copy mode (AC < 16): frames and their element strides
     int64_t row_stride, frame_stride;
+    // batched launch (ssb_deskew_batch, TMA mode): stack b's frames are tensor-map frames
+    // [b*n, (b+1)*n); its outputs sit b strides (elements) past the first stack's
+    int32_t batch;
+    int64_t vol_bstride, xy_bstride, xz_bstride, yz_bstride;
 };
 
 // AC: 16 = rows reach shared memory through one 3-D TMA box (16-byte aligned rows);
@@ -208,11 +212,16 @@ __device__ __forceinline__ void tile_slices(const Params &p, int ut, int64_t &lo
 // Projection-only launches (p.clip) split each tile's own slice range instead of [0, n): a
 // long scan's tile is touched by ~(H + TU)/s of its slices, the rest would be empty stages.
 template <int TU>
-__device__ __forceinline__ void decode(int item, const Params &p, int &ut, int &xt, int64_t &s_begin,
+__device__ __forceinline__ void decode(int item, const Params &p, int &b, int &ut, int &xt, int64_t &s_begin,
                                        int64_t &s_end) {
-    const int items1 = p.UT * p.XT * p.S;
+    // phase 1 of every stack of a batch, then phase 2 of every stack (the tail stays short)
+    const int per1 = p.UT * p.XT * p.S, per2 = p.UT * p.XT * p.S2;
+    const int items1 = per1 * p.batch;
     const bool tail = item >= items1;
     if (tail) item -= items1;
+    const int per = tail ? per2 : per1;
+    b = item / per;
+    item -= b * per;
     const int S = tail ? p.S2 : p.S;
     const int sc = item % S;
     const int rest = item / S;
@@ -788,10 +797,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (++q == kQueue) { q = 0; qphase ^= 1; }
             if (done) break;
-            int ut, xt;
+            int b, ut, xt;
             int64_t s_begin, s_end;
-            decode<kTU>(item, p, ut, xt, s_begin, s_end);
+            decode<kTU>(item, p, b, ut, xt, s_begin, s_end);
             const int64_t tu0 = p.u_begin + (int64_t)ut * kTU;
+            const int32_t frame0 = b * (int32_t)p.n;  // tensor-map frame of this stack's slice 0
             for (int64_t s = s_begin; s < s_end; ++s) {
                 int64_t lo, hi;
                 double off;
@@ -807,7 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (hit && AC == 16) {
                         mbar_expect_tx(&sm.full[stage], kBoxRowsUsed * kRowBytes);
                         tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
-                                    (int32_t)s, policy);
+                                    frame0 + (int32_t)s, policy);
                     }
                 }
                 __syncwarp();
@@ -975,20 +985,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++q == kQueue) { q = 0; qphase ^= 1; }
         if (item < 0) break;
 
-        int ut, xt;
+        int b, ut, xt;
         int64_t s_begin, s_end;
-        decode<kTU>(item, p, ut, xt, s_begin, s_end);
+        decode<kTU>(item, p, b, ut, xt, s_begin, s_end);
         const int64_t x = (int64_t)xt * kTX + lane * 8;
         const bool col_ok = x < p.w;
         const int nv = (int)max((int64_t)0, min((int64_t)8, p.w - x));  // this lane's pixels inside
         const int64_t r0 = (int64_t)ut * kTU + warp * ROWS;  // window row of k = 0
         const int64_t rows_left = p.u_count - r0;
         const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= ROWS ? ROWS : (int)rows_left);
-        uint16_t *vrow = p.vol != nullptr ? p.vol + (size_t)s_begin * plane + (size_t)r0 * p.w + x : nullptr;
+        uint16_t *vrow = p.vol != nullptr ? p.vol + b * p.vol_bstride + (size_t)s_begin * plane + (size_t)r0 * p.w + x
+                                          : nullptr;
         // warp-uniform fast path: every lane's 8 columns and all rows inside the output
         const bool fast = __all_sync(0xffffffffu, AC == 16 ? col_ok : nv == 8) && rows_ok == ROWS;
         // SIDE == false kernels run only without XZ / YZ outputs: their blocks compile away
-        uint32_t *yzp = (SIDE && p.yz != nullptr) ? p.yz + (size_t)s_begin * p.u_count + r0 + lane : nullptr;
+        uint32_t *yzp = (SIDE && p.yz != nullptr) ? p.yz + b * p.yz_bstride + (size_t)s_begin * p.u_count + r0 + lane
+                                                  : nullptr;
         const bool has_xz = SIDE && p.xz != nullptr;
         int g = 0;  // slice within the current XZ batch
 
@@ -1106,7 +1118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int w2 = 0; w2 < kConsumerWarps; ++w2)
                                 red = __vmaxu2(red, sm.xz[((buf * kXzBatch + gg) * kConsumerWarps + w2) * (kTX / 2) + c2]);
-                            uint32_t *dst = p.xz + (size_t)(s0 + gg) * p.w + col;
+                            uint32_t *dst = p.xz + b * p.xz_bstride + (size_t)(s0 + gg) * p.w + col;
                             if (red & 0xFFFFu) red_u32<true>(dst, red & 0xFFFFu);
                             if (red >> 16) red_u32<true>(dst + 1, red >> 16);
                         }
@@ -1116,7 +1128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             uint32_t red = 0;
 #pragma unroll
                             for (int w2 = 0; w2 < kConsumerWarps; ++w2) red += sm.xz[(buf * kConsumerWarps + w2) * kTX + tid];
-                            if (red) red_u32<false>(p.xz + (size_t)s0 * p.w + col, red);
+                            if (red) red_u32<false>(p.xz + b * p.xz_bstride + (size_t)s0 * p.w + col, red);
                         }
                     }
                     ++xz_batch;
@@ -1128,7 +1140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         if (p.xy != nullptr && col_ok) {
-            uint32_t *base = p.xy + (size_t)r0 * p.w + x;
+            uint32_t *base = p.xy + b * p.xy_bstride + (size_t)r0 * p.w + x;
 #pragma unroll
             for (int k = 0; k < ROWS; ++k) {
                 if (k >= rows_ok) break;
@@ -1281,24 +1293,27 @@ int64_t env_i64(const char *name, int64_t dflt) {
 }
 }  // namespace
 
-size_t tma_workspace_bytes(const ssb_deskew_desc &d) {
+size_t tma_workspace_bytes(const ssb_deskew_desc &d, int64_t batch) {
     // u32 reduction scratch for max mode (sum mode reduces straight into the caller's u32 outputs)
     size_t b = kCounterBytes;
     if (d.reduce == SSB_REDUCE_MAX)
-        b += align256((size_t)d.u_count * d.width * 4) + align256((size_t)d.n * d.width * 4) +
-             align256((size_t)d.n * d.u_count * 4);
+        b += align256((size_t)batch * d.u_count * d.width * 4) + align256((size_t)batch * d.n * d.width * 4) +
+             align256((size_t)batch * d.n * d.u_count * 4);
     return b;
 }
 
 int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz, void *yz,
-                      void *workspace, size_t workspace_bytes, cudaStream_t st, int ac) {
+                      void *workspace, size_t workspace_bytes, cudaStream_t st, int ac, int64_t batch) {
     using namespace tma_path;
-    if (workspace == nullptr || workspace_bytes < tma_workspace_bytes(d))
-        return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", tma_workspace_bytes(d),
+    if (batch < 1 || (batch > 1 && ac != 16)) return fail(SSB_ERR_PARAM, "batched launches need TMA-mode stacks");
+    if (batch * d.n > INT32_MAX) return fail(SSB_ERR_CAPACITY, "batch of %lld frames too large", (long long)(batch * d.n));
+    if (workspace == nullptr || workspace_bytes < tma_workspace_bytes(d, batch))
+        return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", tma_workspace_bytes(d, batch),
                     workspace_bytes);
     CUtensorMap map;
     memset(&map, 0, sizeof map);
-    const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)d.n};
+    // a batch is one frame axis of batch * n frames (stacks back to back, frame stride apart)
+    const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)(batch * d.n)};
     const cuuint64_t strides[2] = {(cuuint64_t)row_stride_of(d) * 2, (cuuint64_t)frame_stride_of(d) * 2};
     const bool mx = d.reduce == SSB_REDUCE_MAX;
     const bool side = xz != nullptr || yz != nullptr;
@@ -1325,7 +1340,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     const int sms = num_sms();
     const int64_t UT = std::max<int64_t>(1, (d.u_count + kTU - 1) / kTU);
     const int64_t XT = std::max<int64_t>(1, (d.width + kTX - 1) / kTX);
-    const int64_t tiles = UT * XT;
+    const int64_t tiles = UT * XT * batch;  // tiles of every stack of the batch
     // phase 1: ~SSB_ITEMS_PER_CTA big items per CTA over the first SSB_BIG_PERCENT % of the
     // slices; phase 2: the rest in ~SSB_TAIL_ITEMS_PER_CTA small items
     auto split = [&](int64_t n_sl, int64_t per_cta, int64_t &S, int64_t &chunk) {
@@ -1351,14 +1366,16 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     int64_t S, chunk, S2, chunk2;
     split(n1, per1, S, chunk);
     split(n_plan - n1, env_i64("SSB_TAIL_ITEMS_PER_CTA", 3), S2, chunk2);
-    const int64_t items = tiles * (S + S2);
+    const int64_t items = tiles * (S + S2);  // = batch * UT * XT * (S + S2), decode() order
     if (items > INT32_MAX / 2) return fail(SSB_ERR_CAPACITY, "too many tiles");
 
     char *ws = static_cast<char *>(workspace);
     unsigned int *counters = reinterpret_cast<unsigned int *>(ws);
     ws += kCounterBytes;
     const bool acc = (d.flags & SSB_FLAG_XY_ACCUMULATE) != 0;
-    const size_t n_xy = (size_t)d.u_count * d.width, n_xz = (size_t)d.n * d.width, n_yz = (size_t)d.n * d.u_count;
+    // per stack; the scratch / outputs of a batch hold `batch` of each back to back
+    const size_t s_xy = (size_t)d.u_count * d.width, s_xz = (size_t)d.n * d.width, s_yz = (size_t)d.n * d.u_count;
+    const size_t n_xy = s_xy * batch, n_xz = s_xz * batch, n_yz = s_yz * batch;
     uint32_t *xy32 = nullptr, *xz32 = nullptr, *yz32 = nullptr;
     if (mx) {
         xy32 = xy ? reinterpret_cast<uint32_t *>(ws) : nullptr;
@@ -1413,6 +1430,11 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     prm.raw = raw;
     prm.row_stride = row_stride_of(d);
     prm.frame_stride = frame_stride_of(d);
+    prm.batch = (int32_t)batch;
+    prm.vol_bstride = (int64_t)d.n * d.u_count * d.width;
+    prm.xy_bstride = (int64_t)s_xy;
+    prm.xz_bstride = (int64_t)s_xz;
+    prm.yz_bstride = (int64_t)s_yz;
     const int grid = (int)std::min<int64_t>(items, sms);
 
     int rc;

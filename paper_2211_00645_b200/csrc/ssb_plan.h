@@ -20,7 +20,7 @@ inline int64_t frame_stride_of(const ssb_deskew_desc &d) {
 bool tma_eligible(const ssb_deskew_desc &d, const uint16_t *raw, const void *vol, const void *xy);
 
 // Workspace the TMA path needs (scheduler counter + u32 reduction scratch for max mode).
-size_t tma_workspace_bytes(const ssb_deskew_desc &d);
+size_t tma_workspace_bytes(const ssb_deskew_desc &d, int64_t batch = 1);
 
 // Access class of the persistent kernel for this call: 16 = TMA boxes (16-byte aligned rows);
 // 8 / 4 / 2 = row-copy mode (1-D bulk copies per frame row, AC-byte shared loads and volume
@@ -29,6 +29,6 @@ int persistent_access_class(const ssb_deskew_desc &d, const uint16_t *raw, const
 
 // Launch the persistent kernel (+ scratch resets and the u32 -> u16 finalize).
 int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *vol, void *xy, void *xz, void *yz,
-                      void *workspace, size_t workspace_bytes, cudaStream_t st, int ac);
+                      void *workspace, size_t workspace_bytes, cudaStream_t st, int ac, int64_t batch = 1);
 
 }  // namespace ssb

@@ -205,6 +205,57 @@ def deskew_device(raw: torch.Tensor, shear_px: float, interp: str = "linear", *,
                         canvas_rows=canvas_rows, u_begin=u_begin, u_count=u_count)
 
 
+def deskew_batch(raw: torch.Tensor, shear_px: float, interp: str = "linear", *, formula: str = "canvas",
+                 projection_axes=_AXES, reduce: str = "max", write_volume: bool = True,
+                 volume: torch.Tensor | None = None, projections: dict | None = None,
+                 stream: torch.cuda.Stream | None = None) -> DeskewResult:
+    """Fused deskew + projections of B stacks of one shape in one launch (``ssb_deskew_batch``).
+
+    raw: CUDA uint16 (B, n, H, W), C-contiguous.  Outputs carry a leading batch axis: volume
+    (B, n, U, W); projections 0 -> (B, U, W), 1 -> (B, n, W), 2 -> (B, n, U).  Stack b's outputs
+    equal ``deskew_device(raw[b], ...)``.  Small stacks (config 1) fill the GPU this way instead of
+    one under-occupied launch per stack.
+    """
+    axes = check_options(interp, reduce, formula, projection_axes)
+    if not isinstance(raw, torch.Tensor) or not raw.is_cuda or raw.dtype != torch.uint16 or raw.dim() != 4:
+        raise ParameterError("raw must be a CUDA uint16 (B, n, H, W) tensor")
+    if shear_px < 0:
+        raise ParameterError(f"shear_px must be >= 0, got {shear_px}")
+    raw = raw.contiguous()
+    b, n, h, w = (int(v) for v in raw.shape)
+    if b < 1 or n < 1:
+        raise ParameterError("empty batch")
+    u = canvas_rows_for(n, h, shear_px)
+    dev = raw.device
+    stream = stream or torch.cuda.current_stream(dev)
+    pdt = proj_dtype(reduce)
+    shapes = {0: (b, u, w), 1: (b, n, w), 2: (b, n, u)}
+    projections = dict(projections or {})
+    with torch.cuda.stream(stream):
+        if write_volume and volume is None:
+            volume = torch.empty((b, n, u, w), dtype=torch.uint16, device=dev)
+        if not write_volume:
+            volume = None
+        for a in axes:
+            t = projections.get(a)
+            if t is None:
+                projections[a] = torch.empty(shapes[a], dtype=pdt, device=dev)
+            elif tuple(t.shape) != shapes[a] or t.dtype != pdt or not t.is_contiguous():
+                raise ParameterError(f"projection {a} buffer must be contiguous {shapes[a]} {pdt}")
+        if volume is not None and (tuple(volume.shape) != (b, n, u, w) or volume.dtype != torch.uint16
+                                   or not volume.is_contiguous()):
+            raise ParameterError(f"volume buffer must be contiguous (B, n, U, W) = {(b, n, u, w)} uint16")
+        desc = make_desc(n, h, w, 0, shear_px, interp, formula, 0, u, reduce)
+        lib = _lib.load()
+        ws_bytes = int(lib.ssb_deskew_batch_workspace_bytes(ctypes.byref(desc), b))
+        ws = _workspaces.get(ws_bytes, stream)
+        _lib.check(lib.ssb_deskew_batch(
+            ctypes.byref(desc), b, _vp(raw), _vp(volume), _vp(projections.get(0)), _vp(projections.get(1)),
+            _vp(projections.get(2)), _vp(ws), ctypes.c_size_t(ws.numel()), ctypes.c_void_p(stream.cuda_stream)))
+    return DeskewResult(volume=volume, projections={a: projections[a] for a in axes}, canvas_rows=u, u_begin=0,
+                        u_count=u)
+
+
 def frames_to_array(stack) -> np.ndarray:
     """Accept a list of RawFrame / 2-D arrays or an (n, H, W) array (ss/phantom.py:369-377)."""
     if isinstance(stack, np.ndarray) and stack.ndim == 3:

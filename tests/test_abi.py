@@ -18,7 +18,7 @@ def test_library_builds_and_loads():
     path = _build.build()
     assert os.path.exists(path)
     lib = _lib.load()
-    assert lib.ssb_version() == 100
+    assert lib.ssb_version() == 200
 
 
 def test_exports_every_declared_symbol():
