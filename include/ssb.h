@@ -49,6 +49,10 @@ extern "C" {
 
 /* flags */
 #define SSB_FLAG_XY_ACCUMULATE 1 /* xy = reduce(xy, new) instead of xy = new (canvas place) */
+#define SSB_FLAG_XY_U32 2        /* max mode: xy is the caller's uint32 accumulator, max-folded in place
+                                    (not reset, not narrowed to uint16) -- a chunked stream keeps one
+                                    across its chunks instead of a whole-canvas reset + narrowing pass
+                                    per chunk; frames must take TMA boxes (16-byte aligned, W % 8 == 0) */
 
 typedef struct ssb_deskew_desc {
     int64_t n;           /* frames in this call                                    */

@@ -22,6 +22,7 @@ INTERP = {"nearest": 0, "linear": 1}
 FORMULA = {"canvas": 0, "npinterp": 1}
 REDUCE = {"max": 0, "sum": 1}
 FLAG_XY_ACCUMULATE = 1
+FLAG_XY_U32 = 2
 
 #: every symbol include/ssb.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ssb_version", "ssb_last_error", "ssb_launch_count", "ssb_profile_enable",

@@ -359,10 +359,18 @@ void launch_reduce(const void *src, void *dst, int64_t planes, int64_t m, bool i
 
 using namespace ssb;
 
+__global__ void fold_u16_into_u32_max(const uint16_t *__restrict__ src, uint32_t *__restrict__ dst, int64_t m) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = max(dst[k], (uint32_t)src[k]);
+}
+
 extern "C" size_t ssb_deskew_workspace_bytes(const ssb_deskew_desc *d) {
     if (validate(d) != SSB_OK) return 0;
     const Plan b = make_plan(*d, true, true, true, tiled_rows(*d), false);
-    return std::max(tma_workspace_bytes(*d), kCounterBytes + b.xy_ws + b.xz_ws + b.yz_ws);
+    const size_t base = std::max(tma_workspace_bytes(*d), kCounterBytes + b.xy_ws + b.xz_ws + b.yz_ws);
+    // SSB_FLAG_XY_U32 on the tiled path folds through a uint16 image kept after the scratch
+    const bool xy_u32 = d->reduce == SSB_REDUCE_MAX && (d->flags & SSB_FLAG_XY_U32);
+    return base + (xy_u32 ? align_up((size_t)d->u_count * d->width * 2) : 0);
 }
 
 extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_t *vol, void *xy,
@@ -373,7 +381,7 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
         // nothing placed: projections of an empty window are zero (XY unless accumulating)
         // (and XZ (n, W) / YZ (n, u_count) of an empty window: all-zero rows)
         const size_t esz = d->reduce == SSB_REDUCE_MAX ? 2 : 4;
-        if (xy && !(d->flags & SSB_FLAG_XY_ACCUMULATE))
+        if (xy && !(d->flags & (SSB_FLAG_XY_ACCUMULATE | SSB_FLAG_XY_U32)))
             cudaMemsetAsync(xy, 0, (size_t)d->u_count * d->width * esz, st);
         if (xz) cudaMemsetAsync(xz, 0, (size_t)d->n * d->width * esz, st);
         if (yz) cudaMemsetAsync(yz, 0, (size_t)d->n * d->u_count * esz, st);
@@ -383,8 +391,25 @@ extern "C" int ssb_deskew(const ssb_deskew_desc *d, const uint16_t *raw, uint16_
     // a handful of frames folded into XY only (ProjectionCanvas.place, ss/pipeline.py:316-323) is
     // one small launch of the tiled kernel: no scratch reset, no finalize pass
     const bool tiny = d->n <= 2 && xz == nullptr && yz == nullptr;
-    const int ac = (env_int("SSB_DISABLE_TMA", 0) == 0 && !tiny) ? persistent_access_class(*d, raw, vol, xy) : 0;
+    const bool xy_u32 = d->reduce == SSB_REDUCE_MAX && (d->flags & SSB_FLAG_XY_U32);
+    const int ac = (env_int("SSB_DISABLE_TMA", 0) == 0 && (!tiny || xy_u32)) ? persistent_access_class(*d, raw, vol, xy) : 0;
     if (ac) return launch_deskew_tma(*d, raw, vol, xy, xz, yz, workspace, workspace_bytes, st, ac);
+    if (xy_u32) {
+        // the other paths narrow XY to uint16: run the call into a uint16 image after the scratch,
+        // then max-fold it into the caller's uint32 accumulator
+        ssb_deskew_desc d2 = *d;
+        d2.flags &= ~(SSB_FLAG_XY_U32 | SSB_FLAG_XY_ACCUMULATE);
+        const size_t base = ssb_deskew_workspace_bytes(&d2), m = (size_t)d->u_count * d->width;
+        if (workspace == nullptr || workspace_bytes < base + align_up(m * 2))
+            return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", base + align_up(m * 2),
+                        workspace_bytes);
+        uint16_t *xy16 = reinterpret_cast<uint16_t *>(static_cast<char *>(workspace) + base);
+        if (int rc = ssb_deskew(&d2, raw, vol, xy16, xz, yz, workspace, base, stream)) return rc;
+        const int blocks = (int)std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)num_sms() * 8);
+        fold_u16_into_u32_max<<<std::max(blocks, 1), 256, 0, st>>>(xy16, static_cast<uint32_t *>(xy), (int64_t)m);
+        count_launches(1);
+        return check_launch("fold_u16_into_u32_max");
+    }
 
     const Plan pl = make_plan(*d, xy != nullptr, xz != nullptr, yz != nullptr, tiled_rows(*d), false);
     const size_t need = kCounterBytes + pl.xy_ws + pl.xz_ws + pl.yz_ws;

@@ -1373,12 +1373,13 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     unsigned int *counters = reinterpret_cast<unsigned int *>(ws);
     ws += kCounterBytes;
     const bool acc = (d.flags & SSB_FLAG_XY_ACCUMULATE) != 0;
+    const bool xy_u32 = mx && (d.flags & SSB_FLAG_XY_U32) != 0;  // caller's u32 XY accumulator
     // per stack; the scratch / outputs of a batch hold `batch` of each back to back
     const size_t s_xy = (size_t)d.u_count * d.width, s_xz = (size_t)d.n * d.width, s_yz = (size_t)d.n * d.u_count;
     const size_t n_xy = s_xy * batch, n_xz = s_xz * batch, n_yz = s_yz * batch;
     uint32_t *xy32 = nullptr, *xz32 = nullptr, *yz32 = nullptr;
     if (mx) {
-        xy32 = xy ? reinterpret_cast<uint32_t *>(ws) : nullptr;
+        xy32 = xy ? (xy_u32 ? static_cast<uint32_t *>(xy) : reinterpret_cast<uint32_t *>(ws)) : nullptr;
         ws += align256(n_xy * 4);
         xz32 = xz ? reinterpret_cast<uint32_t *>(ws) : nullptr;
         ws += align256(n_xz * 4);
@@ -1388,13 +1389,17 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
         xz32 = static_cast<uint32_t *>(xz);
         yz32 = static_cast<uint32_t *>(yz);
     }
-    if (mx) {
+    if (mx && !xy_u32) {
         // counter and the u32 scratch are contiguous in the workspace: one memset
         char *end = reinterpret_cast<char *>(counters) + sizeof(unsigned int);
         if (xy32) end = reinterpret_cast<char *>(xy32 + n_xy);
         if (xz32) end = reinterpret_cast<char *>(xz32 + n_xz);
         if (yz32) end = reinterpret_cast<char *>(yz32 + n_yz);
         cudaMemsetAsync(counters, 0, (size_t)(end - reinterpret_cast<char *>(counters)), st);
+    } else if (mx) {  // the caller's XY accumulator keeps its contents
+        cudaMemsetAsync(counters, 0, sizeof(unsigned int), st);
+        if (xz32) cudaMemsetAsync(xz32, 0, n_xz * 4, st);
+        if (yz32) cudaMemsetAsync(yz32, 0, n_yz * 4, st);
     } else {
         cudaMemsetAsync(counters, 0, sizeof(unsigned int), st);
         if (xy32 && !acc) cudaMemsetAsync(xy32, 0, n_xy * 4, st);
@@ -1450,8 +1455,8 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     count_launches(1);
     if (rc) return rc;
 
-    if (mx && (xy32 || xz32 || yz32)) {
-        U16Seg a{xy32, static_cast<uint16_t *>(xy), xy32 ? (int64_t)n_xy : 0, acc ? 1 : 0};
+    if (mx && ((xy32 && !xy_u32) || xz32 || yz32)) {
+        U16Seg a{xy32, static_cast<uint16_t *>(xy), (xy32 && !xy_u32) ? (int64_t)n_xy : 0, acc ? 1 : 0};
         U16Seg b{xz32, static_cast<uint16_t *>(xz), xz32 ? (int64_t)n_xz : 0, 0};
         U16Seg c{yz32, static_cast<uint16_t *>(yz), yz32 ? (int64_t)n_yz : 0, 0};
         const int64_t total = (a.count + b.count + c.count) / 4;

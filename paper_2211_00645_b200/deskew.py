@@ -123,12 +123,12 @@ _workspaces = _Workspaces()
 
 
 def make_desc(n, h, w, first_slice, shear_px, interp, formula, u_begin, u_count, reduce,
-              xy_accumulate=False, row_stride=0, frame_stride=0) -> _lib.DeskewDesc:
+              xy_accumulate=False, row_stride=0, frame_stride=0, xy_u32=False) -> _lib.DeskewDesc:
     return _lib.DeskewDesc(
         n=n, height=h, width=w, first_slice=first_slice, shear_px=float(shear_px),
         interp=_lib.INTERP[interp], formula=_lib.FORMULA[formula], u_begin=u_begin,
         u_count=u_count, reduce=_lib.REDUCE[reduce],
-        flags=_lib.FLAG_XY_ACCUMULATE if xy_accumulate else 0,
+        flags=(_lib.FLAG_XY_ACCUMULATE if xy_accumulate else 0) | (_lib.FLAG_XY_U32 if xy_u32 else 0),
         row_stride=row_stride, frame_stride=frame_stride,
     )
 
@@ -137,7 +137,7 @@ def deskew_device(raw: torch.Tensor, shear_px: float, interp: str = "linear", *,
                   formula: str = "canvas", first_slice: int = 0, canvas_rows: int | None = None,
                   u_begin: int = 0, u_count: int | None = None, projection_axes=_AXES,
                   reduce: str = "max", write_volume: bool = True, volume: torch.Tensor | None = None,
-                  projections: dict | None = None, xy_accumulate: bool = False,
+                  projections: dict | None = None, xy_accumulate: bool = False, xy_u32: bool = False,
                   stream: torch.cuda.Stream | None = None) -> DeskewResult:
     """Fused deskew + projections of device-resident frames (one ``ssb_deskew``).
 
@@ -145,7 +145,9 @@ def deskew_device(raw: torch.Tensor, shear_px: float, interp: str = "linear", *,
     contiguous; rows and frames may be strided (a channel crop of a wider camera frame,
     ss/pipeline.py:105-112, is deskewed in place without a copy).
     Output buffers may be passed in (``volume``, ``projections``) to avoid
-    allocation; ``xy_accumulate`` folds into an existing XY (streaming place).
+    allocation; ``xy_accumulate`` folds into an existing XY (streaming place).  ``xy_u32`` (max
+    mode): ``projections[0]`` is a caller-owned int32 (U, W) accumulator, max-folded in place and
+    never narrowed (``SSB_FLAG_XY_U32``; the chunked streamer keeps one across its chunks).
     """
     axes = check_options(interp, reduce, formula, projection_axes)
     if not isinstance(raw, torch.Tensor) or not raw.is_cuda:
@@ -183,17 +185,20 @@ def deskew_device(raw: torch.Tensor, shear_px: float, interp: str = "linear", *,
             volume = torch.empty((n, u_count, w), dtype=torch.uint16, device=dev)
         if not write_volume:
             volume = None
+        if xy_u32 and (reduce != "max" or 0 not in axes or projections.get(0) is None):
+            raise ParameterError("xy_u32 needs reduce='max' and a caller-owned projections[0] accumulator")
         for a in axes:
             t = projections.get(a)
+            want = torch.int32 if (a == 0 and xy_u32) else pdt
             if t is None:
                 t = (torch.zeros if (a == 0 and xy_accumulate) else torch.empty)(shapes[a], dtype=pdt, device=dev)
                 projections[a] = t
-            elif tuple(t.shape) != shapes[a] or t.dtype != pdt or not t.is_contiguous():
-                raise ParameterError(f"projection {a} buffer must be contiguous {shapes[a]} {pdt}")
+            elif tuple(t.shape) != shapes[a] or t.dtype != want or not t.is_contiguous():
+                raise ParameterError(f"projection {a} buffer must be contiguous {shapes[a]} {want}")
         if volume is not None and (tuple(volume.shape) != (n, u_count, w) or volume.dtype != torch.uint16):
             raise ParameterError(f"volume buffer must be (n, U, W) = {(n, u_count, w)} uint16")
         desc = make_desc(n, h, w, first_slice, shear_px, interp, formula, u_begin, u_count, reduce,
-                         xy_accumulate, row_stride, frame_stride)
+                         xy_accumulate, row_stride, frame_stride, xy_u32)
         lib = _lib.load()
         ws_bytes = int(lib.ssb_deskew_workspace_bytes(ctypes.byref(desc)))
         ws = _workspaces.get(ws_bytes, stream)

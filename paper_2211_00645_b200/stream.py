@@ -181,6 +181,12 @@ class StackStreamer:
                 volume, projs = out.volume, dict(out.projections)
         bounds = self.chunk_bounds(n)
         n_chunks = len(bounds)
+        # max-mode XY: one int32 accumulator for the whole stack (SSB_FLAG_XY_U32), narrowed once
+        # at the end, instead of a whole-canvas scratch reset + narrowing pass per chunk
+        acc32 = None
+        if reduce == "max" and 0 in axes and n_chunks > 1 and w % 8 == 0:
+            with torch.cuda.stream(self.compute_stream):
+                acc32 = torch.zeros((canvas_rows, w), dtype=torch.int32, device=dev)
         for c, (c0, c1) in enumerate(bounds):
             b = c % self.n_buffers
             m = c1 - c0
@@ -204,7 +210,7 @@ class StackStreamer:
             self.compute_stream.wait_event(copied)
             chunk_projs = {}
             if 0 in axes:
-                chunk_projs[0] = projs[0]
+                chunk_projs[0] = projs[0] if acc32 is None else acc32
             if 1 in axes:
                 chunk_projs[1] = projs[1][c0:c1]
             if 2 in axes:
@@ -213,11 +219,14 @@ class StackStreamer:
                           first_slice=first_slice + c0, canvas_rows=canvas_rows,
                           projection_axes=axes, reduce=reduce, write_volume=write_volume,
                           volume=None if volume is None else volume[c0:c1],
-                          projections=chunk_projs, xy_accumulate=c > 0,
-                          stream=self.compute_stream)
+                          projections=chunk_projs, xy_accumulate=c > 0 and acc32 is None,
+                          xy_u32=acc32 is not None, stream=self.compute_stream)
             done = torch.cuda.Event()
             done.record(self.compute_stream)
             self._done[b] = done
+        if acc32 is not None:
+            with torch.cuda.stream(self.compute_stream):
+                projs[0].copy_(acc32)  # values <= 65535: exact narrowing
         current = torch.cuda.current_stream(dev)
         current.wait_stream(self.compute_stream)
         for t in [volume, *projs.values()]:
