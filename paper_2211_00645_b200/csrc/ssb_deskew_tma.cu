@@ -1205,6 +1205,8 @@ __global__ void finalize_u16_kernel(U16Seg s0, U16Seg s1, U16Seg s2) {
 
 // --------------------------------------------------------------------------- host
 
+// cuTensorMapEncodeTiled is a driver entry point, the same for every device: resolved once per
+// process.  (Tensor maps themselves are encoded per call, for the caller's buffer.)
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;

@@ -36,13 +36,19 @@ inline int check_launch(const char *what) {
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// SM count of the calling thread's current device (cached per device: a process may drive
+// several GPUs, e.g. one host thread per device)
 inline int num_sms() {
-    static int sms = 0;
+    constexpr int kMaxDevices = 64;
+    static int cache[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    int sms = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
     if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
+        __atomic_store_n(&cache[dev], sms, __ATOMIC_RELAXED);
     }
     return sms;
 }
