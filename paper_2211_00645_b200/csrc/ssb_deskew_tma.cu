@@ -741,7 +741,8 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     }
 }
 
-template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
+// VOL = false: projection-only instantiation (no volume store code at all)
+template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC, bool VOL>
 __global__ void __launch_bounds__(kThreads, 1)
     deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
@@ -994,8 +995,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t r0 = (int64_t)ut * kTU + warp * ROWS;  // window row of k = 0
         const int64_t rows_left = p.u_count - r0;
         const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= ROWS ? ROWS : (int)rows_left);
-        uint16_t *vrow = p.vol != nullptr ? p.vol + b * p.vol_bstride + (size_t)s_begin * plane + (size_t)r0 * p.w + x
-                                          : nullptr;
+        uint16_t *vrow = (VOL && p.vol != nullptr)
+                             ? p.vol + b * p.vol_bstride + (size_t)s_begin * plane + (size_t)r0 * p.w + x
+                             : nullptr;
         // warp-uniform fast path: every lane's 8 columns and all rows inside the output
         const bool fast = __all_sync(0xffffffffu, AC == 16 ? col_ok : nv == 8) && rows_ok == ROWS;
         // SIDE == false kernels run only without XZ / YZ outputs: their blocks compile away
@@ -1221,14 +1223,21 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
-int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
-    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC>;
+template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC, bool VOL>
+int launch_kernel(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
+    auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, VOL>;
     constexpr int smem = (int)sizeof(Smem<ROWS, AC, SIDE>);
     static_assert(smem <= 227 * 1024, "shared memory budget");
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<grid, kThreads, smem, st>>>(map, prm);
     return check_launch("deskew_tma_kernel");
+}
+
+// projection-only calls (no volume) of the TMA mode get the instantiation without store code
+template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
+int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
+    if (AC == 16 && prm.vol == nullptr) return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, false>(map, prm, grid, st);
+    return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, true>(map, prm, grid, st);
 }
 
 // Kernel instantiation for (reduce, tile height, side projections requested):
