@@ -1328,9 +1328,10 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     const cuuint64_t strides[2] = {(cuuint64_t)row_stride_of(d) * 2, (cuuint64_t)frame_stride_of(d) * 2};
     const bool mx = d.reduce == SSB_REDUCE_MAX;
     const bool side = xz != nullptr || yz != nullptr;
-    // 8-row tiles pay only where the per-row XZ/YZ work dominates: projection-only max with side
-    // projections (measured: XY-only is faster with 4-row tiles and their deeper 5-stage ring)
-    const int64_t tall_env = env_i64("SSB_TALL_TILES", 1);  // 0 never, 1 projection-only, 2 always (A/B)
+    // 8-row tiles (A/B knob): since the fp32 lerp and the volume-free instantiations, 4-row tiles with
+    // their deeper ring are faster for every projection-only variant too (3 MIPs 1.174 vs 1.202 ms,
+    // XY+XZ 1.112 vs 1.166, XY+YZ 1.062 vs 1.122; profiles/r02_v4_tall_ab.txt)
+    const int64_t tall_env = env_i64("SSB_TALL_TILES", 0);  // 0 never, 1 projection-only, 2 always
     const bool tall = (vol == nullptr || tall_env == 2) && tall_env != 0 && mx && side && ac == 16;
     const int kTU = tall ? Cfg<8>::kTU : Cfg<4>::kTU;
     const int slack = d.interp == SSB_INTERP_NEAREST ? box_slack<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>()
