@@ -708,7 +708,8 @@ def run_slabs(args, cfg, rank, world, local_rank):
                        "slab_frames": p.count, "slab_rows": p.u_count, "outputs": "XY sum only (projection-only)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_kind": peak_kind, "bytes_per_launch": bytes_launch,
-                         "kernel_ms": kern_ms / max(kern_n, 1)},
+                         "kernel_ms": kern_ms / max(kern_n, 1),
+                         "traffic": lookup_traffic(p.count, h, w, args.interp, "xy", "sum")},
             "gpu_launches": _lib.launch_count() - launches0,
         }), flush=True)
 
