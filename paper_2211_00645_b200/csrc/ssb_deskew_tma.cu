@@ -582,7 +582,10 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                                           const int nv, uint4 (&acc_max)[ROWS],
                                           uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
                                           uint4 &xz_max, uint32_t (&xz_sum)[8], uint32_t (&yzv)[ROWS]) {
-    constexpr bool kStream = ROWS > 4 || !kMax;
+#ifndef SSB_SIDE_STREAM
+#define SSB_SIDE_STREAM 0  // A/B: 4-row max tiles with XZ/YZ consume each row as it is computed
+#endif
+    constexpr bool kStream = ROWS > 4 || !kMax || (SIDE && SSB_SIDE_STREAM);
     constexpr bool kFoldXz = kMax && SIDE && !kStream;  // XZ over the batch with 3-input maxes
     constexpr bool kPairXz = kMax && SIDE && kStream;   // XZ over row pairs with 3-input maxes
     uint4 xz_prev = make_uint4(0, 0, 0, 0);
@@ -896,7 +899,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // frac(off) away from 0 and 1 by 2^-30, |u - off| < 2^20): taps j0 + r, j0 + r + 1
                 // unclamped and f = 1 - phi within (H + 2) * 2^-52
                 bool regular = false;
-                if (AC == 16 && FORMULA == SSB_FORMULA_CANVAS && hit && SSB_REGULAR_STAGES && !kF64 &&
+                // (AC 8: the lanes' 8-byte copies land in the same 16-byte-aligned rows as a TMA box)
+                if ((AC == 16 || AC == 8) && FORMULA == SSB_FORMULA_CANVAS && hit && SSB_REGULAR_STAGES && !kF64 &&
                     (int64_t)(ut + 1) * kTU <= p.u_count && lo <= tu0 && tu0 + kTU - 1 <= hi && p.h < (1 << 20)) {
                     StageP spv;
                     spv.off = off;
@@ -1037,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define SSB_ROWS_PASS(F, CH, RG)                                                                             \
     rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG>(rg, lane_off, tap_base, spv, u0, vrow, p.w, rows_ok, \
                                                             col_ok, nv, acc_max, acc_sum, xz_max, xz_sum, yzv)
-                if (AC == 16 && FORMULA == SSB_FORMULA_CANVAS && !kF64 && ((hdr >> 15) & 1u)) {
+                if ((AC == 16 || AC == 8) && FORMULA == SSB_FORMULA_CANVAS && !kF64 && ((hdr >> 15) & 1u)) {
                     // regular stage: taps at fixed box rows, one weight bracket (StageP)
                     StageP spv = sm.sp[stage];
                     spv.j0 += warp * ROWS;  // frame row of tap a of this warp's row 0
@@ -1236,7 +1240,8 @@ int launch_kernel(const CUtensorMap &map, const Params &prm, int grid, cudaStrea
 // projection-only calls (no volume) of the TMA mode get the instantiation without store code
 template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
 int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
-    if (AC == 16 && prm.vol == nullptr) return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, false>(map, prm, grid, st);
+    if ((AC == 16 || AC == 8) && prm.vol == nullptr)
+        return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, false>(map, prm, grid, st);
     return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, true>(map, prm, grid, st);
 }
 
