@@ -217,7 +217,7 @@ def run_reference(args, cfg, rank, world):
         "unit": "GVoxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         # one step = one full stack's worth of the reference's work, extrapolated from the sample
         "ms_per_step": n * u * w / (gv * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u16 in / f64 lerp / u16 out", "data": "synthetic uniform [0,4096)",
+        "vs_baseline": None, "dtype": "u16 in / fp64-exact lerp (fp32 FFMA2 bracket + fp64 fallback) / u16 out", "data": "synthetic uniform [0,4096)",
         "config": {"workload": cfg["name"], "interp": interp, "shear_px": native_shear(cfg["alpha"]),
                    "canvas": [u, w], "outputs": "XY max (ProjectionCanvas: the reference's only output)",
                    "global_batch": 1, "seq_len": n, "stacks_per_s_equiv": gv * 1e9 / (n * u * w),
@@ -505,14 +505,15 @@ def run_ours(args, cfg, rank, world, local_rank):
             "metric": "deskewed GVoxels/s (fused deskew+MIP)", "value": value, "unit": "GVoxels/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u16 in / f64 lerp / u16 out", "data": "synthetic uniform [0,4096), generated on device",
+            "dtype": "u16 in / fp64-exact lerp (fp32 FFMA2 bracket + fp64 fallback) / u16 out", "data": "synthetic uniform [0,4096), generated on device",
             "config": {"workload": cfg["name"], "interp": interp, "shear_px": s, "canvas": [u, w],
                        "outputs": "volume (N,U,W) u16 + XY/XZ/YZ max", "stacks_per_s": world * 1e3 / ms,
                        "global_batch": world, "seq_len": n, "parallelism": f"dp{world} (stacks)", "l2": l2_note,
                        **({"stacks_total": cfg["stacks"], "stacks_per_rank": len(mine),
                            "resident_distinct_stacks_per_rank": len(raws),
-                           "step": "one stack per rank (its next stack of the shard); XY gathered to rank 0 "
-                                   "over NCCL on a side stream, overlapped with the next stack"}
+                           "step": "one stack per rank (its next stack of the shard)" +
+                                   ("; XY gathered to rank 0 over NCCL on a side stream, overlapped with the next "
+                                    "stack" if world > 1 else "")}
                           if timelapse else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -630,7 +631,7 @@ def run_stream(args, cfg, rank, world, local_rank):
         print(json.dumps({
             "metric": "deskewed GVoxels/s and stacks/s (live-view stream, pinned H2D)", "value": world * vox / (ms * 1e-3) / 1e9,
             "unit": "GVoxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 in / f64 lerp / u16 out",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 in / fp64-exact lerp (fp32 FFMA2 bracket + fp64 fallback) / u16 out",
             "data": "synthetic uniform [0,4096) in pinned host memory",
             "config": {"workload": cfg["name"], "interp": args.interp, "canvas": [u, w], "stacks_per_s": 1e3 / ms,
                        "latency_ms_last_chunk_to_host": lat, "chunk_frames": streamer.chunk, "tail_frames": streamer.tail,
@@ -702,7 +703,7 @@ def run_slabs(args, cfg, rank, world, local_rank):
         print(json.dumps({
             "metric": "deskewed GVoxels/s (long scan, scan-axis slabs, sum projection)", "value": vox / (ms * 1e-3) / 1e9,
             "unit": "GVoxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16 in / f64 lerp / u32 sum",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16 in / fp64-exact lerp (fp32 FFMA2 bracket + fp64 fallback) / u32 sum",
             "data": "synthetic uniform [0,4096), generated on device",
             "config": {"workload": cfg["name"], "interp": args.interp, "canvas": [U, w],
                        "slab_frames": p.count, "slab_rows": p.u_count, "outputs": "XY sum only (projection-only)"},
