@@ -217,7 +217,7 @@ def run_reference(args, cfg, rank, world):
         "unit": "GVoxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         # one step = one full stack's worth of the reference's work, extrapolated from the sample
         "ms_per_step": n * u * w / (gv * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u16 in / fp64-exact lerp (fp32 FFMA2 bracket + fp64 fallback) / u16 out", "data": "synthetic uniform [0,4096)",
+        "vs_baseline": None, "dtype": "u16 in / f64 lerp (numpy) / u16 out", "data": "synthetic uniform [0,4096)",
         "config": {"workload": cfg["name"], "interp": interp, "shear_px": native_shear(cfg["alpha"]),
                    "canvas": [u, w], "outputs": "XY max (ProjectionCanvas: the reference's only output)",
                    "global_batch": 1, "seq_len": n, "stacks_per_s_equiv": gv * 1e9 / (n * u * w),
