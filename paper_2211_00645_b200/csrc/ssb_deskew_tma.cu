@@ -64,6 +64,12 @@ __host__ __device__ constexpr int box_slack() {
 #ifndef SSB_L2_PROMO  // A/B knob: L2 promotion of the TMA box loads
 #define SSB_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_128B
 #endif
+#ifndef SSB_ALIGNED_ROW_STORES
+#define SSB_ALIGNED_ROW_STORES 0  // A/B knob: 8-byte-aligned volume rows use 16-byte stores where aligned
+#endif
+#ifndef SSB_LOOKAHEAD_GAP
+#define SSB_LOOKAHEAD_GAP 3  // consumer-copy mode: lookahead = stages - gap (A/B knob)
+#endif
 #ifndef SSB_REGULAR_STAGES
 #define SSB_REGULAR_STAGES 1  // A/B knob: 0 = per-row tables for every stage
 #endif
@@ -132,6 +138,14 @@ struct alignas(16) StageP {
     int32_t j0;    // frame row of tap a of tile row 0
 };
 
+// consumer-copy mode: the frame rows box rows [r_lo, r_hi) of a stage come from row0 + r * row_stride
+struct CopyRec {
+    const uint16_t *row0;  // box row 0, column xt * 256 (may lie outside the frame; only rows in range are read)
+    int32_t r_lo, r_hi;
+    int32_t x0;            // first column of the tile
+    int32_t state;         // 0: no copy (slice misses the tile), 1: copy, 2: past the last stage
+};
+
 struct Params {
     uint16_t *vol;
     uint32_t *xy;  // u32 reduction targets (zeroed, or the caller's sum outputs)
@@ -161,14 +175,23 @@ struct Params {
 // Measured at 512 x 2048 x W (B200): W = 2044 (AC 8) 2.84 ms, 2046 (AC 4) 3.13 ms, 2047 (AC 2)
 // 3.65 ms, against 1.65 ms for TMA boxes at W = 2048 -- the producer's per-row copy issue, not
 // HBM, bounds these modes.
+// AC 8 / 4 (rows 8- / 4-byte aligned): consumer-copy mode -- the consumer warps copy the frame rows of
+// the stage kLookahead stages ahead with 8- / 4-byte cp.async into 16-byte aligned shared-memory rows
+// (the producer only publishes each stage's copy geometry), so the copies get 15 warps' issue slots
+// and memory-level parallelism instead of one producer warp's.  AC 2 (odd widths): one 1-D bulk copy
+// per frame row (its 16-byte-aligned superset) into 528-byte slots.
+template <int AC>
+__host__ __device__ constexpr bool consumer_copy() {
+    return AC == 8 || AC == 4;
+}
 template <int AC>
 __host__ __device__ constexpr int row_pitch() {
-    return AC <= 4 ? kTX + 8 : kTX;
+    return AC == 2 ? kTX + 8 : kTX;
 }
-// shared-memory rows are 16-byte aligned except in bulk-copy mode (AC <= 4)
+// shared-memory rows are 16-byte aligned except in bulk-copy mode (AC 2)
 template <int AC>
 __host__ __device__ constexpr int smem_ac() {
-    return AC <= 4 ? AC : 16;
+    return AC == 2 ? 2 : 16;
 }
 
 template <int ROWS, int AC = 16, bool SIDE = true>
@@ -181,6 +204,8 @@ struct Smem {
                                // bits 17..31: warps whose rows chain their taps; bit 15: regular
                                // stage (taps and weights from sp[], the row table is not written)
     StageP sp[C::kStages];
+    CopyRec cp[C::kStages];     // consumer-copy mode: what to copy into each stage
+    uint64_t geo[C::kStages];   // consumer-copy mode: cp[] of the stage's current use is published
     alignas(16) uint32_t xz[C::kXzWords];
     uint64_t full[C::kStages];
     uint64_t empty[C::kStages];
@@ -452,6 +477,12 @@ __device__ __forceinline__ void stg8(uint16_t *p, const uint4 v) {
     if (AC == 16) {
         stg_cs_v4(p, v);
     } else if (AC == 8) {
+#if SSB_ALIGNED_ROW_STORES
+        if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {  // this row happens to be 16-byte aligned
+            stg_cs_v4(p, v);
+            return;
+        }
+#endif
         asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
         asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p + 4), "r"(v.z), "r"(v.w) : "memory");
     } else if (AC == 4 || (reinterpret_cast<uintptr_t>(p) & 2u) == 0) {
@@ -754,6 +785,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     using C = Cfg<ROWS, SIDE>;
     constexpr int kTU = C::kTU;
     constexpr int kStages = C::kStages;
+    // consumer-copy mode: stages copied ahead of the one processed; copying stage k + D needs every warp
+    // done with stage k + D - kStages, so D < kStages - 1 leaves the warps room to drift apart
+    constexpr int kLookahead = kStages - SSB_LOOKAHEAD_GAP > 0 ? kStages - SSB_LOOKAHEAD_GAP : 1;
     constexpr int kXzBatch = kMax ? C::kXzBatch : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<ROWS, AC, SIDE> &sm = *reinterpret_cast<Smem<ROWS, AC, SIDE> *>(smem_raw);
@@ -762,7 +796,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) {
         for (int k = 0; k < kStages; ++k) {
             // cp.async modes add one asynchronous arrival per producer lane (copies landed)
-            mbar_init(&sm.full[k], AC == 8 ? 64 : 32);
+            // producer lanes (row table) + in consumer-copy mode every consumer lane's cp.async arrival
+            mbar_init(&sm.full[k], consumer_copy<AC>() ? 32 + kConsumerThreads : 32);
+            mbar_init(&sm.geo[k], 1);
             mbar_init(&sm.empty[k], kConsumerWarps);
         }
         for (int k = 0; k < kQueue; ++k) {
@@ -827,34 +863,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 // row-copy mode: tile row 0's first pixel, and per frame row the byte step
                 uint32_t d0 = 0, rs2 = 0;
-                if (AC == 8) {
-                    if (hit) {
-                        // each lane copies its 8 pixels of every frame row inside [0, H) in AC-byte
-                        // pieces (pieces starting at or past the row end are skipped)
-                        const int64_t x0 = (int64_t)xt * kTX + lane * 8;
-                        const int npix = (int)max((int64_t)0, min((int64_t)8, p.w - x0));
-                        const int r_lo = (int)max((int64_t)0, -box_r0);
-                        const int r_hi = (int)min((int64_t)kBoxRowsUsed, p.h - box_r0);
-                        const char *src = reinterpret_cast<const char *>(p.raw) +
-                                          2 * (s * p.frame_stride + (box_r0 + r_lo) * p.row_stride + x0);
-                        const int64_t step = 2 * p.row_stride;
-                        uint32_t dst = smem_addr(&sm.box[stage][r_lo][0]) + 16u * lane;
-                        constexpr int kPix = AC / 2;
-                        for (int r = r_lo; r < r_hi; ++r, src += step, dst += 2u * kTX) {
-#pragma unroll
-                            for (int q = 0; q < 8 / kPix; ++q) {
-                                if (q * kPix < npix)
-                                    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst + q * AC),
-                                                 "l"(src + q * AC), "n"(AC)
-                                                 : "memory");
-                            }
-                        }
+                if (consumer_copy<AC>()) {
+                    // publish what the consumers copy into this stage (they run kLookahead stages behind)
+                    if (lane == 0) {
+                        CopyRec rec;
+                        rec.row0 = p.raw + s * p.frame_stride + box_r0 * p.row_stride + (int64_t)xt * kTX;
+                        rec.r_lo = (int32_t)max((int64_t)0, -box_r0);
+                        rec.r_hi = (int32_t)min((int64_t)kBoxRowsUsed, p.h - box_r0);
+                        rec.x0 = xt * kTX;
+                        rec.state = hit ? 1 : 0;
+                        sm.cp[stage] = rec;
+                        mbar_arrive(&sm.geo[stage]);
                     }
-                    // arrives (no increment) on `full` once this lane's copies have landed
-                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&sm.full[stage]))
-                                 : "memory");
                 }
-                if (AC <= 4) {
+                if (AC == 2) {
                     const uintptr_t a0 = reinterpret_cast<uintptr_t>(p.raw) +
                                          2u * (uintptr_t)(s * p.frame_stride + (int64_t)xt * kTX);
                     d0 = (uint32_t)(a0 & 15u);
@@ -899,8 +921,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // frac(off) away from 0 and 1 by 2^-30, |u - off| < 2^20): taps j0 + r, j0 + r + 1
                 // unclamped and f = 1 - phi within (H + 2) * 2^-52
                 bool regular = false;
-                // (AC 8: the lanes' 8-byte copies land in the same 16-byte-aligned rows as a TMA box)
-                if ((AC == 16 || AC == 8) && FORMULA == SSB_FORMULA_CANVAS && hit && SSB_REGULAR_STAGES && !kF64 &&
+                // (consumer-copy mode: the copies land in the same 16-byte-aligned rows as a TMA box)
+                if ((AC == 16 || consumer_copy<AC>()) && FORMULA == SSB_FORMULA_CANVAS && hit && SSB_REGULAR_STAGES &&
+                    !kF64 &&
                     (int64_t)(ut + 1) * kTU <= p.u_count && lo <= tu0 && tu0 + kTU - 1 <= hi && p.h < (1 << 20)) {
                     StageP spv;
                     spv.off = off;
@@ -971,6 +994,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++stage == kStages) { stage = 0; sphase ^= 1; }
             }
         }
+        if (consumer_copy<AC>()) {
+            // the consumers look kLookahead stages ahead: mark the stages past the last one
+            for (int d = 0; d < kLookahead; ++d) {
+                if (lane == 0) {
+                    mbar_wait(&sm.empty[stage], sphase ^ 1);
+                    sm.cp[stage].state = 2;
+                    mbar_arrive(&sm.geo[stage]);
+                }
+                if (++stage == kStages) { stage = 0; sphase ^= 1; }
+            }
+        }
         return;
     }
 
@@ -978,6 +1012,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t stage = 0, sphase = 0, q = 0, qphase = 0, xz_batch = 0;
     const size_t plane = (size_t)p.u_count * p.w;
     const uint32_t lane_off = lane * 16;
+    // consumer-copy mode: copy this warp's share (rows r with r % 15 == warp) of stage g's box rows,
+    // then arrive on its `full` barrier when the copies have landed
+    uint32_t g_next = 0;  // next stage (in the global stage sequence) to copy for
+    auto copy_stage = [&]() {
+        const uint32_t slot = g_next % kStages;
+        mbar_wait(&sm.geo[slot], (g_next / kStages) & 1u);
+        ++g_next;
+        const CopyRec rec = sm.cp[slot];
+        if (rec.state == 2) return;
+        if (rec.state == 1) {
+            const int64_t xl = (int64_t)rec.x0 + lane * 8;
+            const int npix = (int)max((int64_t)0, min((int64_t)8, p.w - xl));
+            int r = rec.r_lo + ((warp - rec.r_lo) % kConsumerWarps + kConsumerWarps) % kConsumerWarps;
+            const char *src = reinterpret_cast<const char *>(rec.row0 + r * p.row_stride + lane * 8);
+            const int64_t step = 2 * kConsumerWarps * p.row_stride;
+            uint32_t dst = smem_addr(&sm.box[slot][r][0]) + 16u * lane;
+            constexpr int kPiece = AC == 2 ? 8 : AC;  // (AC 2 never takes this path)
+            for (; r < rec.r_hi; r += kConsumerWarps, src += step, dst += 2u * kTX * kConsumerWarps) {
+#pragma unroll
+                for (int q2 = 0; q2 < 16 / kPiece; ++q2) {
+                    if (q2 * (kPiece / 2) < npix)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst + q2 * kPiece),
+                                     "l"(src + q2 * kPiece), "n"(kPiece)
+                                     : "memory");
+                }
+            }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&sm.full[slot]))
+                     : "memory");
+    };
+    if (consumer_copy<AC>())
+        for (int d = 0; d < kLookahead; ++d) copy_stage();
     while (true) {
         int item = 0;
         if (lane == 0) {
@@ -1025,6 +1091,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr bool kBiased = !kMax && INTERP == SSB_INTERP_LINEAR && !kF64;
         uint32_t n_live = 0;
         for (int si = 0; si < ns; ++si) {
+            if (consumer_copy<AC>()) copy_stage();  // the stage kLookahead ahead of this one
             mbar_wait(&sm.full[stage], sphase);
             const uint32_t hdr = sm.hdr[stage];
             const bool live = (hdr >> 16) & (hdr >> warp) & 1u;
@@ -1041,7 +1108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define SSB_ROWS_PASS(F, CH, RG)                                                                             \
     rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG>(rg, lane_off, tap_base, spv, u0, vrow, p.w, rows_ok, \
                                                             col_ok, nv, acc_max, acc_sum, xz_max, xz_sum, yzv)
-                if ((AC == 16 || AC == 8) && FORMULA == SSB_FORMULA_CANVAS && !kF64 && ((hdr >> 15) & 1u)) {
+                if ((AC == 16 || consumer_copy<AC>()) && FORMULA == SSB_FORMULA_CANVAS && !kF64 && ((hdr >> 15) & 1u)) {
                     // regular stage: taps at fixed box rows, one weight bracket (StageP)
                     StageP spv = sm.sp[stage];
                     spv.j0 += warp * ROWS;  // frame row of tap a of this warp's row 0
@@ -1240,7 +1307,7 @@ int launch_kernel(const CUtensorMap &map, const Params &prm, int grid, cudaStrea
 // projection-only calls (no volume) of the TMA mode get the instantiation without store code
 template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
 int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
-    if ((AC == 16 || AC == 8) && prm.vol == nullptr)
+    if ((AC == 16 || consumer_copy<AC>()) && prm.vol == nullptr)
         return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, false>(map, prm, grid, st);
     return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, true>(map, prm, grid, st);
 }
