@@ -86,12 +86,15 @@ struct Cfg {
     static constexpr int kBoxRows = kTU + 4;
     // without side projections the XZ staging buffer is not needed and a deeper ring fits
     static constexpr int kStages = ROWS >= 8 ? 3 : (SIDE ? 5 : SSB_XY_STAGES);
-    static constexpr int kXzBatch = ROWS >= 8 ? 1 : 2;  // max-mode slices per XZ barrier
+#ifndef SSB_XZ_BATCH
+#define SSB_XZ_BATCH 3  // 3: 3 MIPs 1.175 -> 1.154 ms, XY+XZ 1.112 -> 1.092 (profiles/r02_notes.md)
+#endif
+    static constexpr int kXzBatch = ROWS >= 8 ? 1 : SSB_XZ_BATCH;  // max-mode slices per XZ barrier
     static constexpr int kRowWords = (kTU + 31) / 32;   // 32-row groups the producer lanes cover
     // XZ staging: max mode packs u16x2 (kTX/2 words per warp and slice); sum mode (ROWS 4) u32
     static constexpr int kXzWords = !SIDE ? 4
                                     : ROWS >= 8 ? 2 * kXzBatch * kConsumerWarps * (kTX / 2)
-                                                : 2 * kConsumerWarps * kTX;
+                                                : (kXzBatch > 2 ? kXzBatch : 2) * kConsumerWarps * kTX;
     template <int INTERP, int FORMULA>
     static constexpr int box_rows() {
         return kTU + 2 * box_slack<INTERP, FORMULA>();
@@ -662,8 +665,27 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         }
     };
     uint4 vs[kStream ? 1 : ROWS];
+    // batched fallback (rows computed before they are consumed): one branch per pass tests every row's
+    // bracket check, so the rows' instructions form one basic block the scheduler can interleave
+#ifndef SSB_ONE_FALLBACK
+#define SSB_ONE_FALLBACK 1  // A/B knob
+#endif
+    // (XY-only views: 0.794 -> 0.789 ms at config 2; with XZ the longer block was 3 % slower)
+    constexpr bool kOneFb = SSB_ONE_FALLBACK && !kStream && !SIDE;
+    uint32_t chk[ROWS];
     constexpr bool kF64 = !kMax && SIDE && INTERP == SSB_INTERP_LINEAR;  // see lerp_biased8_raw
     constexpr bool chain32 = chain && !kF64, chain64 = chain && kF64 && FORMULA == SSB_FORMULA_CANVAS;
+    // exact fp64 evaluation of row k (the fp32 bracket's fallback)
+    auto exact_row = [&](const int k, uint32_t (&bits)[8]) {
+        const uint4 ta = lds8<smem_ac<AC>()>(tap_a(k)), tb = lds8<smem_ac<AC>()>(tap_b(k));
+        if (REG) {
+            // canvas formula, unclamped taps j0+k, j0+k+1: f = fl(fl(u - off) - j0), w0 = 1 - f
+            const double f = __dsub_rn(__dsub_rn((double)(u0 + k), sp.off), (double)(sp.j0 + k));
+            exact8<FORMULA>(ta, tb, __dsub_rn(1.0, f), f, 2, bits);
+        } else {
+            exact8<FORMULA>(ta, tb, rg[k].c0, rg[k].c1, rg[k].kind, bits);
+        }
+    };
     f32x2 prev[4];
     double prevd[8];
     if (chain32) to_f23(lds8<smem_ac<AC>()>(tap_a(0)), prev);
@@ -726,16 +748,8 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                 whi = f2pack(wq.z, wq.w);
             }
             uint32_t bits[8];
-            if (lerp8_f32(A, B, wlo, whi, bits) != 0) {
-                const uint4 ta = lds8<smem_ac<AC>()>(tap_a(k)), tb = lds8<smem_ac<AC>()>(tap_b(k));
-                if (REG) {
-                    // canvas formula, unclamped taps j0+k, j0+k+1: f = fl(fl(u - off) - j0), w0 = 1 - f
-                    const double f = __dsub_rn(__dsub_rn((double)(u0 + k), sp.off), (double)(sp.j0 + k));
-                    exact8<FORMULA>(ta, tb, __dsub_rn(1.0, f), f, 2, bits);
-                } else {
-                    exact8<FORMULA>(ta, tb, rg[k].c0, rg[k].c1, rg[k].kind, bits);
-                }
-            }
+            chk[k] = lerp8_f32(A, B, wlo, whi, bits);
+            if (!kOneFb && chk[k] != 0) exact_row(k, bits);
             if (chain32) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) prev[q] = B[q];
@@ -766,6 +780,21 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         else vs[k] = kEdge ? mask_cols(v, nv) : v;
     }
     if (!kStream) {
+        if (kOneFb && INTERP == SSB_INTERP_LINEAR && !kF64) {
+            uint32_t any = 0;
+#pragma unroll
+            for (int k = 0; k < ROWS; ++k) any |= chk[k];
+            if (any != 0) {
+#pragma unroll
+                for (int k = 0; k < ROWS; ++k) {
+                    if (chk[k] != 0) {
+                        uint32_t bits[8];
+                        exact_row(k, bits);
+                        vs[k] = kEdge ? mask_cols(pack8(bits), nv) : pack8(bits);
+                    }
+                }
+            }
+        }
         if (kFoldXz) {
 #pragma unroll
             for (int k = 0; k + 1 < ROWS; k += 2) xz_max = max3_u16x8(xz_max, vs[k], vs[k + 1]);
@@ -789,6 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // done with stage k + D - kStages, so D < kStages - 1 leaves the warps room to drift apart
     constexpr int kLookahead = kStages - SSB_LOOKAHEAD_GAP > 0 ? kStages - SSB_LOOKAHEAD_GAP : 1;
     constexpr int kXzBatch = kMax ? C::kXzBatch : 1;
+    static_assert(kXzBatch * (kTX / 2) <= kConsumerThreads, "one consumer thread per (slice, column pair)");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<ROWS, AC, SIDE> &sm = *reinterpret_cast<Smem<ROWS, AC, SIDE> *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -830,6 +860,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) item = (int)atomicAdd(&p.counters[0], 1u);
             item = __shfl_sync(0xffffffffu, item, 0);
             const bool done = item >= p.n_items;
+            int b = 0, ut = 0, xt = 0;
+            int64_t s_begin = 0, s_end = 0;
+            if (!done) {
+                decode<kTU>(item, p, b, ut, xt, s_begin, s_end);
+                if (s_begin >= s_end) continue;  // items without slices (clipped tiles) are not handed over
+            }
             if (lane == 0) {
                 mbar_wait(&sm.qempty[q], qphase ^ 1);
                 sm.queue[q] = done ? -1 : item;
@@ -837,9 +873,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (++q == kQueue) { q = 0; qphase ^= 1; }
             if (done) break;
-            int b, ut, xt;
-            int64_t s_begin, s_end;
-            decode<kTU>(item, p, b, ut, xt, s_begin, s_end);
             const int64_t tu0 = p.u_begin + (int64_t)ut * kTU;
             const int32_t frame0 = b * (int32_t)p.n;  // tensor-map frame of this stack's slice 0
             for (int64_t s = s_begin; s < s_end; ++s) {
