@@ -21,13 +21,16 @@
 //  * int->double conversion is folded into the products: fma(w, 2^52 + a,
 //    -w*2^52) == fl(w*a) exactly (one rounding), so a voxel costs 2 DFMA + 2 DADD;
 //  * rows that are not 16-byte aligned (W % 8 != 0, odd-offset crops) run the same pipeline
-//    in row-copy mode (template AC < 16): cp.async or per-row 1-D bulk copies instead of the
-//    TMA box, narrower shared loads / volume stores, right-edge lanes masked (see Smem).
+//    in row-class TMA mode (template AC = 32 + alignment, canvas lerp): one tensor map per residue
+//    class of rows (P = 16 / gcd(2 * row_stride, 16) classes), P boxes per stage, 248-column tiles;
+//    nearest, batched or otherwise ineligible calls take the row-copy modes (AC < 16: cp.async or
+//    per-row 1-D bulk copies instead of the TMA box).  Both use narrower shared loads / volume stores.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <numeric>
 
 #include "ssb_plan.h"
 
@@ -167,6 +170,8 @@ struct Params {
     // [b*n, (b+1)*n); its outputs sit b strides (elements) past the first stack's
     int32_t batch;
     int64_t vol_bstride, xy_bstride, xz_bstride, yz_bstride;
+    int32_t rt_P, rt_B;  // row-class TMA: classes and box rows per class
+    uint32_t rt_d0;      // row-class TMA: byte offset (mod 16) of frame row 0 (delta_c = (d0 + c*rs2) & 15)
 };
 
 // AC: 16 = rows reach shared memory through one 3-D TMA box (16-byte aligned rows);
@@ -175,43 +180,89 @@ struct Params {
 // 4 / 2 = rows 4- / 2-byte aligned: one 1-D bulk copy per frame row of its 16-byte-aligned
 // superset into a 528-byte slot, the row table points each tap at its first pixel inside the slot
 // and consumers read with 4- / 2-byte granularity.  Volume stores use AC-byte accesses.
-// Measured at 512 x 2048 x W (B200): W = 2044 (AC 8) 2.84 ms, 2046 (AC 4) 3.13 ms, 2047 (AC 2)
-// 3.65 ms, against 1.65 ms for TMA boxes at W = 2048 -- the producer's per-row copy issue, not
-// HBM, bounds these modes.
+// Measured at 512 x 2048 x W (B200, volume + 3 MIPs): row-copy W = 2044 (AC 8) 2.59 ms, 2046 (AC 4)
+// 2.81 ms, 2047 (AC 2) 3.66 ms; row-class TMA 2.04 / 2.15 / 2.98 ms; TMA boxes at W = 2048 1.60 ms.
 // AC 8 / 4 (rows 8- / 4-byte aligned): consumer-copy mode -- the consumer warps copy the frame rows of
 // the stage kLookahead stages ahead with 8- / 4-byte cp.async into 16-byte aligned shared-memory rows
 // (the producer only publishes each stage's copy geometry), so the copies get 15 warps' issue slots
 // and memory-level parallelism instead of one producer warp's.  AC 2 (odd widths): one 1-D bulk copy
 // per frame row (its 16-byte-aligned superset) into 528-byte slots.
+//
+// Row-class TMA mode (AC = 32 + row alignment: 40 / 36 / 34), the default for rows that are not 16-byte
+// aligned: with P = 16 / gcd(2 * row_stride, 16), the frame rows j = c (mod P) of class c all sit at the
+// same byte offset delta_c (mod 16), so class c gets its own tensor map over every P-th row, based at its
+// first row rounded down to 16 bytes (pixel x of a class-c row is map column x + delta_c / 2).  A stage
+// loads one 256-column box per class at the tile's map column (16-byte aligned), class after class
+// (B rows each); tiles are 248 columns wide so that every class's box covers them (lane 31 idles: in
+// max mode it duplicates lane 30's columns, in sum mode its voxels are masked to zero).  Consumers read
+// taps at the rows' alignment (delta_c); stores keep the volume's.  No per-row copy instructions at all.
 template <int AC>
 __host__ __device__ constexpr bool consumer_copy() {
     return AC == 8 || AC == 4;
 }
 template <int AC>
+__host__ __device__ constexpr bool rt_mode() {
+    return AC > 16;
+}
+// alignment (bytes) of the frame-row taps in shared memory and of the volume rows
+template <int AC>
+__host__ __device__ constexpr int acl() {
+    return AC > 16 ? AC - 32 : AC;
+}
+// columns per tile
+template <int AC>
+__host__ __device__ constexpr int tile_w() {
+    return rt_mode<AC>() ? kTX - 8 : kTX;
+}
+template <int AC>
 __host__ __device__ constexpr int row_pitch() {
     return AC == 2 ? kTX + 8 : kTX;
 }
-// shared-memory rows are 16-byte aligned except in bulk-copy mode (AC 2)
+// shared-memory rows are 16-byte aligned except in bulk-copy mode (AC 2) and row-class TMA mode
 template <int AC>
 __host__ __device__ constexpr int smem_ac() {
-    return AC == 2 ? 2 : 16;
+    return AC == 2 ? 2 : rt_mode<AC>() ? acl<AC>() : 16;
 }
+// row-class TMA: box rows per class for P classes (a stage needs box_rows consecutive frame rows from
+// any start; the class boxes start at the multiple of P at or below it)
+__host__ __device__ constexpr int rt_class_rows(int box_rows, int P) {
+    return (box_rows + 2 * P - 2) / P;
+}
+// shared-memory box rows per stage
+template <int ROWS, bool SIDE, int AC>
+__host__ __device__ constexpr int box_rows_alloc() {
+    return rt_mode<AC>() ? (16 / acl<AC>()) * rt_class_rows(Cfg<ROWS, SIDE>::kTU + 2, 16 / acl<AC>())
+                         : Cfg<ROWS, SIDE>::kBoxRows;
+}
+// ring depth: the 4- / 8-class boxes take more rows per stage than one box
+template <int ROWS, bool SIDE, int AC>
+__host__ __device__ constexpr int stage_count() {
+    return rt_mode<AC>() && acl<AC>() < 8 ? Cfg<ROWS, SIDE>::kStages - 1 : Cfg<ROWS, SIDE>::kStages;
+}
+
+// tensor maps of one launch: [0] the frame box (TMA mode) or the row classes (row-class TMA mode)
+struct alignas(64) TmapSet {
+    CUtensorMap m[8];
+};
 
 template <int ROWS, int AC = 16, bool SIDE = true>
 struct Smem {
     using C = Cfg<ROWS, SIDE>;
-    uint16_t box[C::kStages][C::kBoxRows][row_pitch<AC>()];
+    static constexpr int kStages = stage_count<ROWS, SIDE, AC>();
+    uint16_t box[kStages][box_rows_alloc<ROWS, SIDE, AC>()][row_pitch<AC>()];
     uint16_t zero_row[kTX + 8];
-    RowP rows[C::kStages][C::kTU];
-    uint32_t hdr[C::kStages];  // bit 16: slice touches the tile; bits 0..14: warps with live rows;
+    // row-class TMA, regular stages: shared address of tap rows j0 + i of the stage (no lane offset)
+    alignas(16) uint32_t taddr[rt_mode<AC>() ? kStages : 1][rt_mode<AC>() ? C::kTU + 4 : 4];
+    RowP rows[kStages][C::kTU];
+    uint32_t hdr[kStages];  // bit 16: slice touches the tile; bits 0..14: warps with live rows;
                                // bits 17..31: warps whose rows chain their taps; bit 15: regular
                                // stage (taps and weights from sp[], the row table is not written)
-    StageP sp[C::kStages];
-    CopyRec cp[C::kStages];     // consumer-copy mode: what to copy into each stage
-    uint64_t geo[C::kStages];   // consumer-copy mode: cp[] of the stage's current use is published
+    StageP sp[kStages];
+    CopyRec cp[kStages];     // consumer-copy mode: what to copy into each stage
+    uint64_t geo[kStages];   // consumer-copy mode: cp[] of the stage's current use is published
     alignas(16) uint32_t xz[C::kXzWords];
-    uint64_t full[C::kStages];
-    uint64_t empty[C::kStages];
+    uint64_t full[kStages];
+    uint64_t empty[kStages];
     uint64_t qfull[kQueue];
     uint64_t qempty[kQueue];
     int32_t queue[kQueue];
@@ -474,6 +525,14 @@ __device__ __forceinline__ uint4 lds8(uint32_t a) {
                       __byte_perm(w3, w4, sel));
 }
 
+// a tap's 8 pixels from shared memory in the kernel's mode
+// (row-class TMA, 4- / 2-byte aligned taps: two conflict-free 16-byte loads and a warp-uniform word
+// shift instead were slower except for XY-only at W = 2047, profiles/r02_notes.md)
+template <int AC>
+__device__ __forceinline__ uint4 ldtap(uint32_t a) {
+    return lds8<smem_ac<AC>()>(a);
+}
+
 // 8 pixels to the volume (streaming stores) at an AC-byte aligned address
 template <int AC>
 __device__ __forceinline__ void stg8(uint16_t *p, const uint4 v) {
@@ -501,6 +560,19 @@ __device__ __forceinline__ void stg8(uint16_t *p, const uint4 v) {
         asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p + 5), "r"(__byte_perm(v.z, v.w, 0x5432)) : "memory");
         asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p + 7), "h"((unsigned short)(v.w >> 16)) : "memory");
     }
+}
+
+// 8 pixels at the widest access this address allows (row-class TMA volume rows: the row alignment cycles
+// with the canvas row, the same for every lane of a warp, so the branches are uniform)
+#ifndef SSB_RT_DYN_STORES
+#define SSB_RT_DYN_STORES 1  // A/B knob
+#endif
+__device__ __forceinline__ void stg8_any(uint16_t *p, const uint4 v) {
+    const uint32_t a = (uint32_t)reinterpret_cast<uintptr_t>(p) & 15u;
+    if (a == 0) stg8<16>(p, v);
+    else if ((a & 7u) == 0) stg8<8>(p, v);
+    else if ((a & 3u) == 0) stg8<4>(p, v);
+    else stg8<2>(p, v);
 }
 
 // the first nv (< 8) pixels of a lane that straddles the right edge (row-copy mode only)
@@ -557,10 +629,27 @@ __device__ __forceinline__ void set_bracket(RowP &o, double w) {
 // the row is live (inside the window and the slice's span).
 // Row-copy mode: frame row j of the slice sits at byte (d0 + 2*j*rs) & 15 of its slot (d0: the
 // alignment of row 0's first pixel of the tile); TMA mode: d0 = rs2 = 0.
+// Shared address of frame row j's first tile pixel (no lane offset).  Row-class TMA: class c = (j - jb) mod P
+// (jb = the class boxes' first frame row, a multiple of P), block row (j - jb) / P, B rows per class.
+struct RtGeo {
+    int64_t jb;
+    uint32_t lp, B;  // log2(P), rows per class box
+};
+template <int AC>
+__device__ __forceinline__ uint32_t row_addr(int64_t j, int64_t box_r0, uint32_t box_addr, uint32_t d0, uint32_t rs2,
+                                             const RtGeo &g) {
+    if (rt_mode<AC>()) {
+        const uint32_t q = (uint32_t)(j - g.jb);
+        const uint32_t c = q & ((1u << g.lp) - 1u), r = q >> g.lp;
+        return box_addr + (c * g.B + r) * (2u * row_pitch<AC>()) + ((d0 + rs2 * (uint32_t)j) & 15u);
+    }
+    return box_addr + (uint32_t)(j - box_r0) * (2u * row_pitch<AC>()) + ((d0 + rs2 * (uint32_t)j) & 15u);
+}
+
 template <int INTERP, int FORMULA, int AC, bool F64>
 __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int64_t lo, int64_t hi, double off,
                                          int64_t h, int64_t box_r0, int64_t box_rows, uint32_t box_addr,
-                                         uint32_t zero_addr, uint32_t d0, uint32_t rs2) {
+                                         uint32_t zero_addr, uint32_t d0, uint32_t rs2, const RtGeo &g) {
     o.c0 = 1.0;
     o.c1 = 0.0;
     o.off_a = o.off_b = zero_addr;
@@ -578,9 +667,8 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     // the box covers [box_r0, box_r0 + TU + 2*slack): a tap outside it would read another
     // stage's data -- fail loudly instead (cheap: once per row per slice, producer warp only)
     if (rp.j0 < box_r0 || rp.j1 < box_r0 || rp.j0 - box_r0 >= box_rows || rp.j1 - box_r0 >= box_rows) __trap();
-    constexpr uint32_t pitch = 2u * row_pitch<AC>();
-    o.off_a = box_addr + (uint32_t)(rp.j0 - box_r0) * pitch + ((d0 + rs2 * (uint32_t)rp.j0) & 15u);
-    o.off_b = box_addr + (uint32_t)(rp.j1 - box_r0) * pitch + ((d0 + rs2 * (uint32_t)rp.j1) & 15u);
+    o.off_a = row_addr<AC>(rp.j0, box_r0, box_addr, d0, rs2, g);
+    o.off_b = row_addr<AC>(rp.j1, box_r0, box_addr, d0, rs2, g);
     if (rp.kind >= 2) {
         o.c0 = rp.c0;
         o.c1 = rp.c1;
@@ -611,7 +699,7 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
 // the fallback re-derives row k's exact weight from the slice offset (canvas row u0 + k, tap j0 + k).
 template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN, int AC, bool REG>
 __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off, const uint32_t tap_base,
-                                          const StageP &sp, const int64_t u0,
+                                          const uint32_t *tad, const StageP &sp, const int64_t u0,
                                           uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
                                           const int nv, uint4 (&acc_max)[ROWS],
                                           uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
@@ -626,14 +714,28 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     const bool store = vrow != nullptr;
     constexpr bool chain = (CHAIN || REG) && INTERP == SSB_INTERP_LINEAR;
     constexpr uint32_t kPitch = 2u * row_pitch<AC>();
+    constexpr bool kRT = rt_mode<AC>();
+    // row-class TMA, regular stage: the rows' tap addresses from the stage's table (consecutive rows
+    // alternate between class boxes)
+    uint32_t ta[ROWS + 1];
+    if (kRT && REG) {
+#pragma unroll
+        for (int k = 0; k <= ROWS; ++k) ta[k] = tad[k] + lane_off;
+    }
     // tap addresses of row k (lane offset included)
-    auto tap_a = [&](const int k) { return REG ? tap_base + (uint32_t)k * kPitch : rg[k].off_a + lane_off; };
-    auto tap_b = [&](const int k) { return REG ? tap_base + (uint32_t)(k + 1) * kPitch : rg[k].off_b + lane_off; };
-    constexpr bool kEdge = AC != 16 && !FULL;  // a lane may straddle the right edge
+    auto tap_a = [&](const int k) {
+        return REG ? (kRT ? ta[k] : tap_base + (uint32_t)k * kPitch) : rg[k].off_a + lane_off;
+    };
+    auto tap_b = [&](const int k) {
+        return REG ? (kRT ? ta[k + 1] : tap_base + (uint32_t)(k + 1) * kPitch) : rg[k].off_b + lane_off;
+    };
+    // a lane may straddle the right edge; row-class TMA sums also mask lane 31 (max mode duplicates lane 30)
+    constexpr bool kEdge = (AC != 16 && !FULL) || (kRT && !kMax);
     auto put = [&](const int k, const uint4 v) {
-        if (!(store && (FULL || (k < rows_ok && col_ok)))) return;
+        if (!(store && (FULL ? (!kRT || col_ok) : (k < rows_ok && col_ok)))) return;
         if (kEdge && nv < 8) stg_partial(vrow + k * w, v, nv);
-        else stg8<AC>(vrow + k * w, v);
+        else if (kRT && SSB_RT_DYN_STORES && acl<AC>() == 8) stg8_any(vrow + k * w, v);
+        else stg8<acl<AC>()>(vrow + k * w, v);
     };
     auto consume = [&](const int k, uint4 v) {
         if (kEdge) v = mask_cols(v, nv);
@@ -647,7 +749,13 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                 } else if (!kFoldXz) {
                     xz_max = max_u16x8(xz_max, v);
                 }
+#if defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 5  // timing experiment only: no CREDUX
+                yzv[k] = hmax8(v);
+#elif defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 6  // timing experiment only: no YZ work
+                yzv[k] = 0;
+#else
                 yzv[k] = redux_max(hmax8(v));
+#endif
             }
         } else {
             const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
@@ -677,7 +785,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     constexpr bool chain32 = chain && !kF64, chain64 = chain && kF64 && FORMULA == SSB_FORMULA_CANVAS;
     // exact fp64 evaluation of row k (the fp32 bracket's fallback)
     auto exact_row = [&](const int k, uint32_t (&bits)[8]) {
-        const uint4 ta = lds8<smem_ac<AC>()>(tap_a(k)), tb = lds8<smem_ac<AC>()>(tap_b(k));
+        const uint4 ta = ldtap<AC>(tap_a(k)), tb = ldtap<AC>(tap_b(k));
         if (REG) {
             // canvas formula, unclamped taps j0+k, j0+k+1: f = fl(fl(u - off) - j0), w0 = 1 - f
             const double f = __dsub_rn(__dsub_rn((double)(u0 + k), sp.off), (double)(sp.j0 + k));
@@ -688,8 +796,8 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     };
     f32x2 prev[4];
     double prevd[8];
-    if (chain32) to_f23(lds8<smem_ac<AC>()>(tap_a(0)), prev);
-    if (chain64) to_biased8(lds8<smem_ac<AC>()>(tap_a(0)), prevd);
+    if (chain32) to_f23(ldtap<AC>(tap_a(0)), prev);
+    if (chain64) to_biased8(ldtap<AC>(tap_a(0)), prevd);
     f32x2 wlo_s = 0, whi_s = 0;
     if (REG) {
         wlo_s = f2pack(__float_as_uint(sp.w_lo), __float_as_uint(sp.w_lo));
@@ -699,7 +807,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     for (int k = 0; k < ROWS; ++k) {
         uint4 v;
         if (INTERP == SSB_INTERP_NEAREST) {
-            v = lds8<smem_ac<AC>()>(tap_a(k));
+            v = ldtap<AC>(tap_a(k));
         } else if (kF64) {
             // the producer writes full row tables for these kernels (no regular stages)
             uint32_t bits[8];
@@ -707,13 +815,13 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
             const int kind = rg[k].kind;
             if (chain64) {
                 double cur[8];
-                to_biased8(lds8<smem_ac<AC>()>(tap_b(k)), cur);
+                to_biased8(ldtap<AC>(tap_b(k)), cur);
                 uint32_t r[8];
                 lerp_biased8_raw(prevd, cur, c0, c1, rg[k].n0, rg[k].n1, bits);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) prevd[c] = cur[c];
             } else {
-                exact8<FORMULA>(lds8<smem_ac<AC>()>(tap_a(k)), lds8<smem_ac<AC>()>(tap_b(k)), c0, c1, kind, bits);
+                exact8<FORMULA>(ldtap<AC>(tap_a(k)), ldtap<AC>(tap_b(k)), c0, c1, kind, bits);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) bits[c] &= 0xFFFFu;  // unbiased: these kernels sum plain voxels
             }
@@ -734,12 +842,12 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
             // fp32 bracket of the lerp (RowP); chained taps: tap row k+1 is tap b of row k and
             // tap a of row k+1, converted once
             f32x2 A[4], B[4];
-            to_f23(lds8<smem_ac<AC>()>(tap_b(k)), B);
+            to_f23(ldtap<AC>(tap_b(k)), B);
             if (chain32) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) A[q] = prev[q];
             } else {
-                to_f23(lds8<smem_ac<AC>()>(tap_a(k)), A);
+                to_f23(ldtap<AC>(tap_a(k)), A);
             }
             f32x2 wlo = wlo_s, whi = whi_s;
             if (!REG) {
@@ -797,7 +905,9 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         }
         if (kFoldXz) {
 #pragma unroll
+#if !(defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 4)  // 4: timing experiment only, no XZ fold
             for (int k = 0; k + 1 < ROWS; k += 2) xz_max = max3_u16x8(xz_max, vs[k], vs[k + 1]);
+#endif
         }
 #pragma unroll
         for (int k = 0; k < ROWS; ++k) consume(k, vs[k < (kStream ? 1 : ROWS) ? k : 0]);
@@ -807,13 +917,16 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
 // VOL = false: projection-only instantiation (no volume store code at all)
 template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC, bool VOL>
 __global__ void __launch_bounds__(kThreads, 1)
-    deskew_tma_kernel(const __grid_constant__ CUtensorMap tmap, const Params p) {
+    deskew_tma_kernel(const __grid_constant__ TmapSet maps, const Params p) {
     constexpr bool kMax = REDUCE == SSB_REDUCE_MAX;
     // sum mode with XZ / YZ evaluates voxels in fp64 (see lerp_biased8_raw) from full row tables
     constexpr bool kF64 = !kMax && SIDE && INTERP == SSB_INTERP_LINEAR;
     using C = Cfg<ROWS, SIDE>;
     constexpr int kTU = C::kTU;
-    constexpr int kStages = C::kStages;
+    constexpr int kStages = stage_count<ROWS, SIDE, AC>();
+    constexpr bool kRT = rt_mode<AC>();
+    constexpr int kTW = tile_w<AC>();  // columns per tile
+    const CUtensorMap &tmap = maps.m[0];
     // consumer-copy mode: stages copied ahead of the one processed; copying stage k + D needs every warp
     // done with stage k + D - kStages, so D < kStages - 1 leaves the warps room to drift apart
     constexpr int kLookahead = kStages - SSB_LOOKAHEAD_GAP > 0 ? kStages - SSB_LOOKAHEAD_GAP : 1;
@@ -842,7 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == kConsumerWarps) {
         // ===================== producer warp =====================
-        if (lane == 0) prefetch_tmap(&tmap);
+        if (lane < (kRT ? p.rt_P : 1)) prefetch_tmap(&maps.m[lane]);
         // L2 policy of the frame loads: evict-normal in max mode (measured 2-3 % faster isolated:
         // halo rows shared by vertically adjacent tiles survive), evict-first in sum mode (whose u32
         // REDs into the caller's outputs want the L2 space; evict-normal was 2 % slower there)
@@ -885,6 +998,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // the box load goes out as soon as the stage is free; the row table is built
                 // while it is in flight (full completes on the bytes + all 32 lane arrivals)
                 constexpr int kBoxRowsUsed = C::template box_rows<INTERP, FORMULA>();
+                // row-class TMA: the class boxes start at frame row jb (the multiple of P at or below box_r0)
+                RtGeo rg{0, 0, 0};
+                if (kRT) {
+                    rg.lp = (uint32_t)(__ffs(p.rt_P) - 1);
+                    rg.B = (uint32_t)p.rt_B;
+                    rg.jb = (box_r0 >> rg.lp) << rg.lp;  // floor (arithmetic shift)
+                }
                 if (lane == 0) {
                     mbar_wait(&sm.empty[stage], sphase ^ 1);
                     if (hit && AC == 16) {
@@ -892,10 +1012,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_load_3d(&sm.box[stage][0][0], &tmap, &sm.full[stage], xt * kTX, (int32_t)box_r0,
                                     frame0 + (int32_t)s, policy);
                     }
+                    if (hit && kRT) {
+                        mbar_expect_tx(&sm.full[stage], (uint32_t)(p.rt_P * p.rt_B) * kRowBytes);
+                        for (int c = 0; c < p.rt_P; ++c)
+                            tma_load_3d(&sm.box[stage][c * p.rt_B][0], &maps.m[c], &sm.full[stage], xt * kTW,
+                                        (int32_t)(rg.jb >> rg.lp), (int32_t)s, policy);
+                    }
                 }
                 __syncwarp();
                 // row-copy mode: tile row 0's first pixel, and per frame row the byte step
                 uint32_t d0 = 0, rs2 = 0;
+                if (kRT) {
+                    d0 = p.rt_d0;
+                    rs2 = (uint32_t)((2 * p.row_stride) & 15);
+                }
                 if (consumer_copy<AC>()) {
                     // publish what the consumers copy into this stage (they run kLookahead stages behind)
                     if (lane == 0) {
@@ -955,8 +1085,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // unclamped and f = 1 - phi within (H + 2) * 2^-52
                 bool regular = false;
                 // (consumer-copy mode: the copies land in the same 16-byte-aligned rows as a TMA box)
-                if ((AC == 16 || consumer_copy<AC>()) && FORMULA == SSB_FORMULA_CANVAS && hit && SSB_REGULAR_STAGES &&
-                    !kF64 &&
+                if ((AC == 16 || consumer_copy<AC>() || kRT) && FORMULA == SSB_FORMULA_CANVAS && hit &&
+                    SSB_REGULAR_STAGES && !kF64 &&
                     (int64_t)(ut + 1) * kTU <= p.u_count && lo <= tu0 && tu0 + kTU - 1 <= hi && p.h < (1 << 20)) {
                     StageP spv;
                     spv.off = off;
@@ -979,6 +1109,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                             spv.j0 = (int32_t)j0;
                         }
                     }
+                    if (regular && kRT) {
+                        // tap rows j0 .. j0 + kTU of the stage: their shared addresses (two per lane)
+                        const uint32_t box_addr = smem_addr(&sm.box[stage][0][0]);
+#pragma unroll
+                        for (int j = 0; j < (kTU + 1 + 31) / 32; ++j) {
+                            const int i = lane + 32 * j;
+                            if (i <= kTU) sm.taddr[stage][i] = row_addr<AC>(spv.j0 + i, box_r0, box_addr, d0, rs2, rg);
+                        }
+                    }
                     if (regular && lane == 0) {
                         sm.sp[stage] = spv;
                         sm.hdr[stage] = 0x7FFFu | (1u << 15) | (1u << 16) | (0x7FFFu << 17);
@@ -998,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             l = make_row<INTERP, FORMULA, AC, kF64>(sm.rows[stage][r], tu0 + r,
                                                               (int64_t)ut * kTU + r < p.u_count, lo, hi, off, p.h,
                                                               box_r0, C::template box_rows<INTERP, FORMULA>(),
-                                                              box_addr, zero_addr, d0, rs2);
+                                                              box_addr, zero_addr, d0, rs2, rg);
                         live[j] = __ballot_sync(0xffffffffu, l);
                     }
                 }
@@ -1044,7 +1183,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== consumer warps =====================
     uint32_t stage = 0, sphase = 0, q = 0, qphase = 0, xz_batch = 0;
     const size_t plane = (size_t)p.u_count * p.w;
-    const uint32_t lane_off = lane * 16;
+    // row-class TMA, max mode: lane 31 (outside the 248-column tile) duplicates lane 30's columns
+    const uint32_t lane_off = (kRT && kMax ? min(lane, 30) : lane) * 16;
     // consumer-copy mode: copy this warp's share (rows r with r % 15 == warp) of stage g's box rows,
     // then arrive on its `full` barrier when the copies have landed
     uint32_t g_next = 0;  // next stage (in the global stage sequence) to copy for
@@ -1092,9 +1232,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int b, ut, xt;
         int64_t s_begin, s_end;
         decode<kTU>(item, p, b, ut, xt, s_begin, s_end);
-        const int64_t x = (int64_t)xt * kTX + lane * 8;
-        const bool col_ok = x < p.w;
-        const int nv = (int)max((int64_t)0, min((int64_t)8, p.w - x));  // this lane's pixels inside
+        const int64_t x = (int64_t)xt * kTW + lane * 8;
+        const bool col_ok = x < p.w && (!kRT || lane < 31);
+        // this lane's pixels inside (row-class TMA: lane 31 has none)
+        const int nv = (kRT && lane == 31) ? 0 : (int)max((int64_t)0, min((int64_t)8, p.w - x));
         const int64_t r0 = (int64_t)ut * kTU + warp * ROWS;  // window row of k = 0
         const int64_t rows_left = p.u_count - r0;
         const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= ROWS ? ROWS : (int)rows_left);
@@ -1102,7 +1243,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                              ? p.vol + b * p.vol_bstride + (size_t)s_begin * plane + (size_t)r0 * p.w + x
                              : nullptr;
         // warp-uniform fast path: every lane's 8 columns and all rows inside the output
-        const bool fast = __all_sync(0xffffffffu, AC == 16 ? col_ok : nv == 8) && rows_ok == ROWS;
+        const bool fast =
+            __all_sync(0xffffffffu, AC == 16 ? col_ok : (nv == 8 || (kRT && lane == 31))) && rows_ok == ROWS;
         // SIDE == false kernels run only without XZ / YZ outputs: their blocks compile away
         uint32_t *yzp = (SIDE && p.yz != nullptr) ? p.yz + b * p.yz_bstride + (size_t)s_begin * p.u_count + r0 + lane
                                                   : nullptr;
@@ -1139,12 +1281,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool chained = (hdr >> (17 + warp)) & 1u;
                 const int64_t u0 = p.u_begin + r0;  // canvas row of this warp's row 0
 #define SSB_ROWS_PASS(F, CH, RG)                                                                             \
-    rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG>(rg, lane_off, tap_base, spv, u0, vrow, p.w, rows_ok, \
+    rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG>(rg, lane_off, tap_base, tad, spv, u0, vrow, p.w, rows_ok, \
                                                             col_ok, nv, acc_max, acc_sum, xz_max, xz_sum, yzv)
-                if ((AC == 16 || consumer_copy<AC>()) && FORMULA == SSB_FORMULA_CANVAS && !kF64 && ((hdr >> 15) & 1u)) {
+                if ((AC == 16 || consumer_copy<AC>() || kRT) && FORMULA == SSB_FORMULA_CANVAS && !kF64 &&
+                    ((hdr >> 15) & 1u)) {
                     // regular stage: taps at fixed box rows, one weight bracket (StageP)
                     StageP spv = sm.sp[stage];
                     spv.j0 += warp * ROWS;  // frame row of tap a of this warp's row 0
+                    const uint32_t *tad = kRT ? &sm.taddr[stage][warp * ROWS] : nullptr;
                     const uint32_t tap_base = smem_addr(&sm.box[stage][0][0]) +
                                               (uint32_t)(spv.a0 + warp * ROWS) * (2u * row_pitch<AC>()) + lane_off;
                     if (fast) SSB_ROWS_PASS(true, true, true);
@@ -1152,6 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                     const StageP spv{};
                     const uint32_t tap_base = 0;
+                    const uint32_t *tad = nullptr;
                     // four specialisations so the row loop has no per-row branches
                     if (fast) {
                         if (chained) SSB_ROWS_PASS(true, true, false);
@@ -1168,7 +1313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < ROWS; ++k) {
                     if (k >= rows_ok) continue;
                     if (AC != 16 && nv < 8) stg_partial(vrow + (size_t)k * p.w, z, nv);
-                    else stg8<AC>(vrow + (size_t)k * p.w, z);
+                    else stg8<acl<AC>()>(vrow + (size_t)k * p.w, z);
                 }
             }
             __syncwarp();
@@ -1213,23 +1358,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *reinterpret_cast<uint4 *>(dst + 4) = make_uint4(xz_sum[4], xz_sum[5], xz_sum[6], xz_sum[7]);
                 }
                 if (g == kXzBatch - 1 || si + 1 == ns) {
+#if !(defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 3)  // 3: timing experiment only, no barrier
                     named_bar_sync(1, kConsumerThreads);
+#endif
                     const int64_t s0 = s_begin + si - g;  // first slice of this batch
                     if (kMax) {
                         // thread -> (slice of batch, word of 2 columns)
                         const int gg = tid / (kTX / 2), c2 = tid % (kTX / 2);
-                        const int64_t col = (int64_t)xt * kTX + 2 * c2;
-                        if (gg <= g && col < p.w) {
+                        const int64_t col = (int64_t)xt * kTW + 2 * c2;
+                        if (gg <= g && 2 * c2 < kTW && col < p.w) {
                             uint32_t red = 0;
 #pragma unroll
                             for (int w2 = 0; w2 < kConsumerWarps; ++w2)
                                 red = __vmaxu2(red, sm.xz[((buf * kXzBatch + gg) * kConsumerWarps + w2) * (kTX / 2) + c2]);
                             uint32_t *dst = p.xz + b * p.xz_bstride + (size_t)(s0 + gg) * p.w + col;
+#if defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 1  // timing experiment only: plain stores
+                            if (red) *reinterpret_cast<uint2 *>(dst) = make_uint2(red & 0xFFFFu, red >> 16);
+#elif defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 2  // timing experiment only: no output
+                            if (red == 0xFFFFFFFFu && col < 0) red_u32<true>(dst, red);
+#else
                             if (red & 0xFFFFu) red_u32<true>(dst, red & 0xFFFFu);
                             if (red >> 16) red_u32<true>(dst + 1, red >> 16);
+#endif
                         }
-                    } else if (tid < kTX) {
-                        const int64_t col = (int64_t)xt * kTX + tid;
+                    } else if (tid < kTW) {
+                        const int64_t col = (int64_t)xt * kTW + tid;
                         if (col < p.w) {
                             uint32_t red = 0;
 #pragma unroll
@@ -1328,7 +1481,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC, bool VOL>
-int launch_kernel(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
+int launch_kernel(const TmapSet &map, const Params &prm, int grid, cudaStream_t st) {
     auto kern = deskew_tma_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, VOL>;
     constexpr int smem = (int)sizeof(Smem<ROWS, AC, SIDE>);
     static_assert(smem <= 227 * 1024, "shared memory budget");
@@ -1339,8 +1492,8 @@ int launch_kernel(const CUtensorMap &map, const Params &prm, int grid, cudaStrea
 
 // projection-only calls (no volume) of the TMA mode get the instantiation without store code
 template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
-int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t st) {
-    if ((AC == 16 || consumer_copy<AC>()) && prm.vol == nullptr)
+int launch_one(const TmapSet &map, const Params &prm, int grid, cudaStream_t st) {
+    if ((AC == 16 || consumer_copy<AC>() || rt_mode<AC>()) && prm.vol == nullptr)
         return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, false>(map, prm, grid, st);
     return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, true>(map, prm, grid, st);
 }
@@ -1349,7 +1502,7 @@ int launch_one(const CUtensorMap &map, const Params &prm, int grid, cudaStream_t
 //   max: 4 rows {with, without XZ/YZ}, 8 rows with XZ/YZ (projection-only, TMA mode only)
 //   sum: 4 rows {with, without}
 template <int INTERP, int FORMULA, int AC>
-int launch_variant(bool mx, bool tall, bool side, const CUtensorMap &map, const Params &prm, int grid,
+int launch_variant(bool mx, bool tall, bool side, const TmapSet &map, const Params &prm, int grid,
                    cudaStream_t st) {
     if (mx) {
         if (side) {
@@ -1363,13 +1516,18 @@ int launch_variant(bool mx, bool tall, bool side, const CUtensorMap &map, const 
 }
 
 template <int INTERP, int FORMULA>
-int launch_ac(int ac, bool mx, bool tall, bool side, const CUtensorMap &map, const Params &prm, int grid,
+int launch_ac(int ac, bool mx, bool tall, bool side, const TmapSet &map, const Params &prm, int grid,
               cudaStream_t st) {
     if (ac == 16) return launch_variant<INTERP, FORMULA, 16>(mx, tall, side, map, prm, grid, st);
     if constexpr (FORMULA == SSB_FORMULA_CANVAS) {  // row-copy mode: canvas formula (ProjectionCanvas) only
         if (ac == 8) return launch_variant<INTERP, FORMULA, 8>(mx, false, side, map, prm, grid, st);
         if (ac == 4) return launch_variant<INTERP, FORMULA, 4>(mx, false, side, map, prm, grid, st);
         if (ac == 2) return launch_variant<INTERP, FORMULA, 2>(mx, false, side, map, prm, grid, st);
+        if constexpr (INTERP == SSB_INTERP_LINEAR) {  // row-class TMA (AC = 32 + row alignment)
+            if (ac == 40) return launch_variant<INTERP, FORMULA, 40>(mx, false, side, map, prm, grid, st);
+            if (ac == 36) return launch_variant<INTERP, FORMULA, 36>(mx, false, side, map, prm, grid, st);
+            if (ac == 34) return launch_variant<INTERP, FORMULA, 34>(mx, false, side, map, prm, grid, st);
+        }
     }
     return fail(SSB_ERR_PARAM, "no persistent kernel for access class %d", ac);
 }
@@ -1426,8 +1584,9 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     if (workspace == nullptr || workspace_bytes < tma_workspace_bytes(d, batch))
         return fail(SSB_ERR_CAPACITY, "workspace too small: need %zu bytes, got %zu", tma_workspace_bytes(d, batch),
                     workspace_bytes);
-    CUtensorMap map;
-    memset(&map, 0, sizeof map);
+    TmapSet maps;
+    memset(&maps, 0, sizeof maps);
+    CUtensorMap &map = maps.m[0];
     // a batch is one frame axis of batch * n frames (stacks back to back, frame stride apart)
     const cuuint64_t dims[3] = {(cuuint64_t)d.width, (cuuint64_t)d.height, (cuuint64_t)(batch * d.n)};
     const cuuint64_t strides[2] = {(cuuint64_t)row_stride_of(d) * 2, (cuuint64_t)frame_stride_of(d) * 2};
@@ -1451,12 +1610,45 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
                                        SSB_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SSB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
+    // Rows that are not 16-byte aligned (canvas lerp, one stack, frames 16 bytes apart): one tensor map per
+    // row class (see rt_mode) instead of the row-copy modes.  P = 16 / gcd(2 * row_stride, 16) classes.
+    int32_t rt_P = 0, rt_B = 0;
+    uint32_t rt_d0 = 0;
+    {
+        const int64_t rs = row_stride_of(d), fs = frame_stride_of(d);
+        const int64_t rs16 = (2 * rs) % 16;
+        const int P = rs16 == 0 ? 1 : 16 / (int)std::gcd<int64_t>(rs16, 16);
+        if (ac < 16 && d.formula == SSB_FORMULA_CANVAS && d.interp == SSB_INTERP_LINEAR && batch == 1 &&
+            (2 * fs) % 16 == 0 && d.height >= P && P <= 16 / ac && encode_fn() != nullptr &&
+            env_i64("SSB_DISABLE_RT", 0) == 0) {
+            const uintptr_t r0 = reinterpret_cast<uintptr_t>(raw);
+            const int B = rt_class_rows(rows, P);
+            bool ok = true;
+            for (int c = 0; c < P && ok; ++c) {
+                const uintptr_t a = r0 + 2u * (uintptr_t)(c * rs), dlt = a & 15u;
+                const cuuint64_t cd[3] = {(cuuint64_t)(d.width + (int64_t)dlt / 2),
+                                          (cuuint64_t)((d.height - c + P - 1) / P), (cuuint64_t)d.n};
+                const cuuint64_t cs[2] = {(cuuint64_t)(2 * P * rs), (cuuint64_t)(2 * fs)};
+                const cuuint32_t cb[3] = {(cuuint32_t)kTX, (cuuint32_t)B, 1};
+                ok = encode_fn()(&maps.m[c], CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, reinterpret_cast<void *>(a - dlt), cd, cs,
+                                 cb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, SSB_L2_PROMO,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            }
+            if (ok) {
+                rt_P = P;
+                rt_B = B;
+                rt_d0 = (uint32_t)(r0 & 15u);
+                ac += 32;
+            }
+        }
+    }
 
     // work items: (u-tile, x-tile, slice chunk); ~kItemsPerCta items per persistent CTA keep the
     // dynamic scheduler's tail short (projections reduce in L2, so chunking costs no partial planes)
     const int sms = num_sms();
     const int64_t UT = std::max<int64_t>(1, (d.u_count + kTU - 1) / kTU);
-    const int64_t XT = std::max<int64_t>(1, (d.width + kTX - 1) / kTX);
+    const int64_t tw = ac > 16 ? kTX - 8 : kTX;  // tile width (row-class TMA: 248)
+    const int64_t XT = std::max<int64_t>(1, (d.width + tw - 1) / tw);
     const int64_t tiles = UT * XT * batch;  // tiles of every stack of the batch
     // phase 1: ~SSB_ITEMS_PER_CTA big items per CTA over the first SSB_BIG_PERCENT % of the
     // slices; phase 2: the rest in ~SSB_TAIL_ITEMS_PER_CTA small items
@@ -1557,17 +1749,20 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     prm.xy_bstride = (int64_t)s_xy;
     prm.xz_bstride = (int64_t)s_xz;
     prm.yz_bstride = (int64_t)s_yz;
+    prm.rt_P = rt_P;
+    prm.rt_B = rt_B;
+    prm.rt_d0 = rt_d0;
     const int grid = (int)std::min<int64_t>(items, sms);
 
     int rc;
     profile_begin(st);
     // one place decides the instantiation, consistent with the tile height planned above
     if (d.interp == SSB_INTERP_NEAREST)
-        rc = launch_ac<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>(ac, mx, tall, side, map, prm, grid, st);
+        rc = launch_ac<SSB_INTERP_NEAREST, SSB_FORMULA_CANVAS>(ac, mx, tall, side, maps, prm, grid, st);
     else if (d.formula == SSB_FORMULA_CANVAS)
-        rc = launch_ac<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>(ac, mx, tall, side, map, prm, grid, st);
+        rc = launch_ac<SSB_INTERP_LINEAR, SSB_FORMULA_CANVAS>(ac, mx, tall, side, maps, prm, grid, st);
     else
-        rc = launch_ac<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>(ac, mx, tall, side, map, prm, grid, st);
+        rc = launch_ac<SSB_INTERP_LINEAR, SSB_FORMULA_NPINTERP>(ac, mx, tall, side, maps, prm, grid, st);
     profile_end(st);
     count_launches(1);
     if (rc) return rc;

@@ -594,11 +594,14 @@ def test_generic_path_vector_widths(w, offset):
                 np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
 
 
+@pytest.mark.parametrize("rt", [True, False], ids=["rowclass_tma", "row_copy"])
 @pytest.mark.parametrize("seed", range(8))
-def test_row_copy_mode_randomized(seed):
-    """Rows that are not 16-byte aligned take the persistent kernel's row-copy mode (8-byte cp.async
-    or per-row bulk copies): random widths, strided crops at odd offsets, slab windows, both
-    reductions, volume and projection-only, forced narrower access classes -- all bit-exact."""
+def test_row_copy_mode_randomized(seed, rt):
+    """Rows that are not 16-byte aligned take the persistent kernel's row-class TMA mode (one tensor map
+    per row residue class, 248-column tiles) or, with SSB_DISABLE_RT=1 (and for nearest), its row-copy
+    mode (8-byte cp.async or per-row bulk copies): random widths, strided crops at odd offsets, slab
+    windows, both reductions, volume and projection-only, forced narrower access classes -- all
+    bit-exact."""
     rng = np.random.default_rng(7700 + seed)
     n, h = int(rng.integers(3, 60)), int(rng.integers(1, 80))
     w = int(rng.integers(1, 700))
@@ -614,6 +617,8 @@ def test_row_copy_mode_randomized(seed):
     force = ["", "4", "2"][seed % 3]
     old = os.environ.get("SSB_FORCE_AC")
     os.environ["SSB_FORCE_AC"] = force
+    if not rt:
+        os.environ["SSB_DISABLE_RT"] = "1"
     try:
         for interp in ("linear", "nearest"):
             for reduce in ("max", "sum"):
@@ -633,10 +638,39 @@ def test_row_copy_mode_randomized(seed):
                 for ax in (0, 1, 2):
                     np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), O.project(ref, ax, reduce))
     finally:
+        os.environ.pop("SSB_DISABLE_RT", None)
         if old is None:
             os.environ.pop("SSB_FORCE_AC", None)
         else:
             os.environ["SSB_FORCE_AC"] = old
+
+
+@pytest.mark.parametrize("w", [2044, 2046, 2047, 1020, 499])
+@pytest.mark.parametrize("rt", [True, False], ids=["rowclass_tma", "row_copy"])
+def test_odd_width_wide_frames(w, rt):
+    """Wide frames whose rows are 8-, 4- or 2-byte aligned: many 248-column tiles (row-class TMA) or
+    256-column tiles (row-copy), regular and irregular stages, against the C oracle."""
+    rng = np.random.default_rng(w)
+    n, h, s = 40, 200, 0.8660254037844386
+    st = rng.integers(0, 4096, (n, h, w)).astype(np.uint16)
+    raw = torch.from_numpy(st).to(dev())
+    if not rt:
+        os.environ["SSB_DISABLE_RT"] = "1"
+    try:
+        for reduce in ("max", "sum"):
+            want_vol, want = C.deskew(st, s, "linear", reduce=reduce)
+            res = deskew_device(raw, s, "linear", reduce=reduce)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
+            for ax in (0, 1, 2):
+                np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
+            for axes in ((0,), (0, 1, 2)):
+                res = deskew_device(raw, s, "linear", reduce=reduce, write_volume=False, projection_axes=axes)
+                torch.cuda.synchronize()
+                for ax in axes:
+                    np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
+    finally:
+        os.environ.pop("SSB_DISABLE_RT", None)
 
 
 def test_deskew_graph_replay_matches_direct_calls():
