@@ -21,9 +21,9 @@
 //  * int->double conversion is folded into the products: fma(w, 2^52 + a,
 //    -w*2^52) == fl(w*a) exactly (one rounding), so a voxel costs 2 DFMA + 2 DADD;
 //  * rows that are not 16-byte aligned (W % 8 != 0, odd-offset crops) run the same pipeline
-//    in row-class TMA mode (template AC = 32 + alignment, canvas lerp): one tensor map per residue
+//    in row-class TMA mode (template AC = 32 + alignment, canvas formula): one tensor map per residue
 //    class of rows (P = 16 / gcd(2 * row_stride, 16) classes), P boxes per stage, 248-column tiles;
-//    nearest, batched or otherwise ineligible calls take the row-copy modes (AC < 16: cp.async or
+//    batched or otherwise ineligible calls take the row-copy modes (AC < 16: cp.async or
 //    per-row 1-D bulk copies instead of the TMA box).  Both use narrower shared loads / volume stores.
 #include <algorithm>
 #include <cstdlib>
@@ -1523,11 +1523,10 @@ int launch_ac(int ac, bool mx, bool tall, bool side, const TmapSet &map, const P
         if (ac == 8) return launch_variant<INTERP, FORMULA, 8>(mx, false, side, map, prm, grid, st);
         if (ac == 4) return launch_variant<INTERP, FORMULA, 4>(mx, false, side, map, prm, grid, st);
         if (ac == 2) return launch_variant<INTERP, FORMULA, 2>(mx, false, side, map, prm, grid, st);
-        if constexpr (INTERP == SSB_INTERP_LINEAR) {  // row-class TMA (AC = 32 + row alignment)
-            if (ac == 40) return launch_variant<INTERP, FORMULA, 40>(mx, false, side, map, prm, grid, st);
-            if (ac == 36) return launch_variant<INTERP, FORMULA, 36>(mx, false, side, map, prm, grid, st);
-            if (ac == 34) return launch_variant<INTERP, FORMULA, 34>(mx, false, side, map, prm, grid, st);
-        }
+        // row-class TMA (AC = 32 + row alignment)
+        if (ac == 40) return launch_variant<INTERP, FORMULA, 40>(mx, false, side, map, prm, grid, st);
+        if (ac == 36) return launch_variant<INTERP, FORMULA, 36>(mx, false, side, map, prm, grid, st);
+        if (ac == 34) return launch_variant<INTERP, FORMULA, 34>(mx, false, side, map, prm, grid, st);
     }
     return fail(SSB_ERR_PARAM, "no persistent kernel for access class %d", ac);
 }
@@ -1618,7 +1617,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
         const int64_t rs = row_stride_of(d), fs = frame_stride_of(d);
         const int64_t rs16 = (2 * rs) % 16;
         const int P = rs16 == 0 ? 1 : 16 / (int)std::gcd<int64_t>(rs16, 16);
-        if (ac < 16 && d.formula == SSB_FORMULA_CANVAS && d.interp == SSB_INTERP_LINEAR && batch == 1 &&
+        if (ac < 16 && d.formula == SSB_FORMULA_CANVAS && batch == 1 &&
             (2 * fs) % 16 == 0 && d.height >= P && P <= 16 / ac && encode_fn() != nullptr &&
             env_i64("SSB_DISABLE_RT", 0) == 0) {
             const uintptr_t r0 = reinterpret_cast<uintptr_t>(raw);

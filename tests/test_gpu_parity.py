@@ -598,7 +598,7 @@ def test_generic_path_vector_widths(w, offset):
 @pytest.mark.parametrize("seed", range(8))
 def test_row_copy_mode_randomized(seed, rt):
     """Rows that are not 16-byte aligned take the persistent kernel's row-class TMA mode (one tensor map
-    per row residue class, 248-column tiles) or, with SSB_DISABLE_RT=1 (and for nearest), its row-copy
+    per row residue class, 248-column tiles) or, with SSB_DISABLE_RT=1, its row-copy
     mode (8-byte cp.async or per-row bulk copies): random widths, strided crops at odd offsets, slab
     windows, both reductions, volume and projection-only, forced narrower access classes -- all
     bit-exact."""
@@ -657,15 +657,15 @@ def test_odd_width_wide_frames(w, rt):
     if not rt:
         os.environ["SSB_DISABLE_RT"] = "1"
     try:
-        for reduce in ("max", "sum"):
-            want_vol, want = C.deskew(st, s, "linear", reduce=reduce)
-            res = deskew_device(raw, s, "linear", reduce=reduce)
+        for interp, reduce in (("linear", "max"), ("linear", "sum"), ("nearest", "max")):
+            want_vol, want = C.deskew(st, s, interp, reduce=reduce)
+            res = deskew_device(raw, s, interp, reduce=reduce)
             torch.cuda.synchronize()
             np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
             for ax in (0, 1, 2):
                 np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
             for axes in ((0,), (0, 1, 2)):
-                res = deskew_device(raw, s, "linear", reduce=reduce, write_volume=False, projection_axes=axes)
+                res = deskew_device(raw, s, interp, reduce=reduce, write_volume=False, projection_axes=axes)
                 torch.cuda.synchronize()
                 for ax in axes:
                     np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
