@@ -749,13 +749,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                 } else if (!kFoldXz) {
                     xz_max = max_u16x8(xz_max, v);
                 }
-#if defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 5  // timing experiment only: no CREDUX
-                yzv[k] = hmax8(v);
-#elif defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 6  // timing experiment only: no YZ work
-                yzv[k] = 0;
-#else
                 yzv[k] = redux_max(hmax8(v));
-#endif
             }
         } else {
             const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
@@ -905,9 +899,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
         }
         if (kFoldXz) {
 #pragma unroll
-#if !(defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 4)  // 4: timing experiment only, no XZ fold
             for (int k = 0; k + 1 < ROWS; k += 2) xz_max = max3_u16x8(xz_max, vs[k], vs[k + 1]);
-#endif
         }
 #pragma unroll
         for (int k = 0; k < ROWS; ++k) consume(k, vs[k < (kStream ? 1 : ROWS) ? k : 0]);
@@ -1358,9 +1350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *reinterpret_cast<uint4 *>(dst + 4) = make_uint4(xz_sum[4], xz_sum[5], xz_sum[6], xz_sum[7]);
                 }
                 if (g == kXzBatch - 1 || si + 1 == ns) {
-#if !(defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 3)  // 3: timing experiment only, no barrier
                     named_bar_sync(1, kConsumerThreads);
-#endif
                     const int64_t s0 = s_begin + si - g;  // first slice of this batch
                     if (kMax) {
                         // thread -> (slice of batch, word of 2 columns)
@@ -1372,14 +1362,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int w2 = 0; w2 < kConsumerWarps; ++w2)
                                 red = __vmaxu2(red, sm.xz[((buf * kXzBatch + gg) * kConsumerWarps + w2) * (kTX / 2) + c2]);
                             uint32_t *dst = p.xz + b * p.xz_bstride + (size_t)(s0 + gg) * p.w + col;
-#if defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 1  // timing experiment only: plain stores
-                            if (red) *reinterpret_cast<uint2 *>(dst) = make_uint2(red & 0xFFFFu, red >> 16);
-#elif defined(SSB_XZ_EXPERIMENT) && SSB_XZ_EXPERIMENT == 2  // timing experiment only: no output
-                            if (red == 0xFFFFFFFFu && col < 0) red_u32<true>(dst, red);
-#else
                             if (red & 0xFFFFu) red_u32<true>(dst, red & 0xFFFFu);
                             if (red >> 16) red_u32<true>(dst + 1, red >> 16);
-#endif
                         }
                     } else if (tid < kTW) {
                         const int64_t col = (int64_t)xt * kTW + tid;
