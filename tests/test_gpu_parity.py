@@ -378,6 +378,26 @@ def test_streamer_chunks_match_single_launch(kernel_path):
                 np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want_r[ax])
 
 
+@pytest.mark.parametrize("w", [300, 301, 298])
+def test_streamer_odd_width_chunks(w):
+    """Chunked streaming (global slice offsets, the uint32 XY accumulator) over rows that are 8-, 2- or
+    4-byte aligned: the row-class TMA mode per chunk equals one launch over the whole stack."""
+    from paper_2211_00645_b200.stream import StackStreamer, pinned_stack
+    rng = np.random.default_rng(w)
+    n, h, s = 29, 44, 0.8660254037844386
+    st = rng.integers(0, 65536, (n, h, w)).astype(np.uint16)
+    pin = pinned_stack(n, h, w)
+    pin[:] = st
+    for interp in ("linear", "nearest"):
+        for reduce in ("max", "sum"):
+            want_vol, want = C.deskew(st, s, interp, reduce=reduce)
+            res = StackStreamer(h, w, chunk_frames=6).run(pin, s, interp, reduce=reduce)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(res.volume.cpu().numpy(), want_vol)
+            for ax in (0, 1, 2):
+                np.testing.assert_array_equal(res.projections[ax].cpu().numpy(), want[ax])
+
+
 def test_deskew_volume_host_api():
     rng = np.random.default_rng(8)
     st = rng.integers(0, 4096, (12, 20, 40)).astype(np.uint16)
