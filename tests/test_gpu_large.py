@@ -3,7 +3,7 @@
 Config 1 (128 x 256 x 512) is checked voxel for voxel against the C oracle; config 3
 (200 x 1024 x 1024) through the pinned streaming pipeline against the oracle's projections.
 Config 2 (512 x 2048 x 2048, the headline) is checked voxel for voxel against the C oracle
-(in 64-slice chunks) and with size-independent
+(in 64-slice chunks; also at W = 2044 / 2047, the row-class TMA mode) and with size-independent
 properties: sampled slices against the oracle (global slice index, full canvas
 row window), every projection against a reduction of the kernel's own volume,
 and the XY canvas against the oracle's streaming canvas.
@@ -102,6 +102,27 @@ def test_config2_full_volume_voxel_for_voxel(interp):
     plus every projection against the oracle's."""
     n, h, w, U = 512, 2048, 2048, 2491
     raw = synthetic(n, h, w, 5, hi=65536)
+    res = deskew_device(raw, S30, interp, reduce="max")
+    torch.cuda.synchronize()
+    assert res.volume.shape == (n, U, w)
+    xy = np.zeros((U, w), np.uint16)
+    for k in range(0, n, 64):
+        st = raw[k:k + 64].cpu().numpy()
+        want_vol, want = C.deskew(st, S30, interp, first_slice=k, u_begin=0, u_count=U)
+        np.testing.assert_array_equal(res.volume[k:k + 64].cpu().numpy(), want_vol, err_msg=f"slices {k}..{k + 63}")
+        np.testing.assert_array_equal(res.projections[1][k:k + 64].cpu().numpy(), want[1])
+        np.testing.assert_array_equal(res.projections[2][k:k + 64].cpu().numpy(), want[2])
+        np.maximum(xy, want[0], out=xy)
+    np.testing.assert_array_equal(res.projections[0].cpu().numpy(), xy)
+
+
+@pytest.mark.parametrize("interp,w", [("linear", 2044), ("nearest", 2044), ("linear", 2047)])
+def test_config2_odd_width_voxel_for_voxel(interp, w):
+    """Config 2's shape with rows that are not 16-byte aligned (W = 2044: 8-byte rows, two row classes;
+    W = 2047: 2-byte rows, eight classes) through the row-class TMA mode: every slice against the C
+    oracle (64-slice chunks, global indices), every projection too."""
+    n, h, U = 512, 2048, 2491
+    raw = synthetic(n, h, w, 7, hi=65536)
     res = deskew_device(raw, S30, interp, reduce="max")
     torch.cuda.synchronize()
     assert res.volume.shape == (n, U, w)
