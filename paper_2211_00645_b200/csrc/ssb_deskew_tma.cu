@@ -528,8 +528,31 @@ __device__ __forceinline__ uint4 lds8(uint32_t a) {
 // a tap's 8 pixels from shared memory in the kernel's mode
 // (row-class TMA, 4- / 2-byte aligned taps: two conflict-free 16-byte loads and a warp-uniform word
 // shift instead were slower except for XY-only at W = 2047, profiles/r02_notes.md)
-template <int AC>
+// 2- / 4-byte aligned taps: three 8-byte loads around the tap (12 shared-memory wavefronts, against 20 / 16
+// for five / four 4-byte loads with the 4-way bank conflicts of a 16-byte lane stride), then a shift by a
+// whole word (a & 4) and, for 2-byte alignment, a half word (a & 2) -- both warp-uniform (the row's)
+// (projection-only kernels: W = 2046 / 2047 XY only 1.143 / 1.377 -> 1.095 / 1.323 ms, 3 MIPs 1.525 / 1.677
+// -> 1.486 / 1.612; with a volume they were 1-2.5 % slower, so volume kernels keep the 4-byte loads)
+#ifndef SSB_RT_W64_LOADS
+#define SSB_RT_W64_LOADS 2  // A/B knob: 0 off, 1 for 2-byte aligned taps, 2 also for 4-byte aligned taps
+#endif
+template <int A>
+__device__ __forceinline__ uint4 lds8_w64(uint32_t a) {
+    const uint32_t b = a & ~7u;
+    const uint2 p = lds64(b), q = lds64(b + 8), r = lds64(b + 16);
+    const bool w = (a & 4u) != 0;
+    const uint32_t v0 = w ? p.y : p.x, v1 = w ? q.x : p.y, v2 = w ? q.y : q.x, v3 = w ? r.x : q.y;
+    if (A == 4) return make_uint4(v0, v1, v2, v3);
+    const uint32_t v4 = w ? r.y : r.x, sel = (a & 2u) ? 0x5432u : 0x3210u;
+    return make_uint4(__byte_perm(v0, v1, sel), __byte_perm(v1, v2, sel), __byte_perm(v2, v3, sel),
+                      __byte_perm(v3, v4, sel));
+}
+
+template <int AC, bool W64 = false>
 __device__ __forceinline__ uint4 ldtap(uint32_t a) {
+    if (W64 && rt_mode<AC>() &&
+        ((acl<AC>() == 2 && SSB_RT_W64_LOADS >= 1) || (acl<AC>() == 4 && SSB_RT_W64_LOADS >= 2)))
+        return lds8_w64<acl<AC>()>(a);
     return lds8<smem_ac<AC>()>(a);
 }
 
@@ -697,7 +720,8 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
 // outside pixels are zeroed before any reduction and never stored.
 // REG: a regular stage (StageP): taps at fixed box rows (tap_base + k rows), one weight bracket,
 // the fallback re-derives row k's exact weight from the slice offset (canvas row u0 + k, tap j0 + k).
-template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN, int AC, bool REG>
+template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN, int AC, bool REG,
+          bool NOVOL>
 __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off, const uint32_t tap_base,
                                           const uint32_t *tad, const StageP &sp, const int64_t u0,
                                           uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
@@ -779,7 +803,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     constexpr bool chain32 = chain && !kF64, chain64 = chain && kF64 && FORMULA == SSB_FORMULA_CANVAS;
     // exact fp64 evaluation of row k (the fp32 bracket's fallback)
     auto exact_row = [&](const int k, uint32_t (&bits)[8]) {
-        const uint4 ta = ldtap<AC>(tap_a(k)), tb = ldtap<AC>(tap_b(k));
+        const uint4 ta = ldtap<AC, NOVOL>(tap_a(k)), tb = ldtap<AC, NOVOL>(tap_b(k));
         if (REG) {
             // canvas formula, unclamped taps j0+k, j0+k+1: f = fl(fl(u - off) - j0), w0 = 1 - f
             const double f = __dsub_rn(__dsub_rn((double)(u0 + k), sp.off), (double)(sp.j0 + k));
@@ -790,8 +814,8 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     };
     f32x2 prev[4];
     double prevd[8];
-    if (chain32) to_f23(ldtap<AC>(tap_a(0)), prev);
-    if (chain64) to_biased8(ldtap<AC>(tap_a(0)), prevd);
+    if (chain32) to_f23(ldtap<AC, NOVOL>(tap_a(0)), prev);
+    if (chain64) to_biased8(ldtap<AC, NOVOL>(tap_a(0)), prevd);
     f32x2 wlo_s = 0, whi_s = 0;
     if (REG) {
         wlo_s = f2pack(__float_as_uint(sp.w_lo), __float_as_uint(sp.w_lo));
@@ -801,7 +825,7 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     for (int k = 0; k < ROWS; ++k) {
         uint4 v;
         if (INTERP == SSB_INTERP_NEAREST) {
-            v = ldtap<AC>(tap_a(k));
+            v = ldtap<AC, NOVOL>(tap_a(k));
         } else if (kF64) {
             // the producer writes full row tables for these kernels (no regular stages)
             uint32_t bits[8];
@@ -809,13 +833,13 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
             const int kind = rg[k].kind;
             if (chain64) {
                 double cur[8];
-                to_biased8(ldtap<AC>(tap_b(k)), cur);
+                to_biased8(ldtap<AC, NOVOL>(tap_b(k)), cur);
                 uint32_t r[8];
                 lerp_biased8_raw(prevd, cur, c0, c1, rg[k].n0, rg[k].n1, bits);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) prevd[c] = cur[c];
             } else {
-                exact8<FORMULA>(ldtap<AC>(tap_a(k)), ldtap<AC>(tap_b(k)), c0, c1, kind, bits);
+                exact8<FORMULA>(ldtap<AC, NOVOL>(tap_a(k)), ldtap<AC, NOVOL>(tap_b(k)), c0, c1, kind, bits);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) bits[c] &= 0xFFFFu;  // unbiased: these kernels sum plain voxels
             }
@@ -836,12 +860,12 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
             // fp32 bracket of the lerp (RowP); chained taps: tap row k+1 is tap b of row k and
             // tap a of row k+1, converted once
             f32x2 A[4], B[4];
-            to_f23(ldtap<AC>(tap_b(k)), B);
+            to_f23(ldtap<AC, NOVOL>(tap_b(k)), B);
             if (chain32) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) A[q] = prev[q];
             } else {
-                to_f23(ldtap<AC>(tap_a(k)), A);
+                to_f23(ldtap<AC, NOVOL>(tap_a(k)), A);
             }
             f32x2 wlo = wlo_s, whi = whi_s;
             if (!REG) {
@@ -1273,7 +1297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool chained = (hdr >> (17 + warp)) & 1u;
                 const int64_t u0 = p.u_begin + r0;  // canvas row of this warp's row 0
 #define SSB_ROWS_PASS(F, CH, RG)                                                                             \
-    rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG>(rg, lane_off, tap_base, tad, spv, u0, vrow, p.w, rows_ok, \
+    rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG, !VOL>(rg, lane_off, tap_base, tad, spv, u0, vrow, p.w, rows_ok, \
                                                             col_ok, nv, acc_max, acc_sum, xz_max, xz_sum, yzv)
                 if ((AC == 16 || consumer_copy<AC>() || kRT) && FORMULA == SSB_FORMULA_CANVAS && !kF64 &&
                     ((hdr >> 15) & 1u)) {
