@@ -598,6 +598,44 @@ __device__ __forceinline__ void stg8_any(uint16_t *p, const uint4 v) {
     else stg8<2>(p, v);
 }
 
+// Row-class TMA volume rows that are 2- or 4-byte aligned: lane l's 16 bytes start r = (address & 15) past a
+// 16-byte boundary.  Lanes 1..30 store the aligned 16 bytes [q - r, q - r + 16) -- the left neighbour's last
+// r bytes and their own first 16 - r -- as one 16-byte store; lanes 0 and 30 also store their own 16 bytes
+// with narrow stores (covering the segment's unaligned head and tail; the overlap rewrites equal bytes).
+// Narrow 2- / 4-byte stores at a 16-byte lane stride write every sector in 4-8 pieces; this writes whole
+// sectors.  r is the same for every lane (lanes are 16 bytes apart), so the branch is uniform.
+// (W = 2047, volume + 3 MIPs: 2.985 -> 2.750 ms; at 4-byte rows (W = 2046) 2.167 -> 2.227, so 2-byte rows only)
+#ifndef SSB_RT_SHIFT_STORES
+#define SSB_RT_SHIFT_STORES 1  // A/B knob
+#endif
+template <int A>
+__device__ __forceinline__ void stg8_shift(uint16_t *q, const uint4 v, const uint32_t ln) {
+    const uint32_t r = (uint32_t)reinterpret_cast<uintptr_t>(q) & 15u;
+    if (r == 0) {
+        if (ln < 31) stg_cs_v4(q, v);
+        return;
+    }
+    const uint32_t W0 = __shfl_up_sync(0xffffffffu, v.x, 1), W1 = __shfl_up_sync(0xffffffffu, v.y, 1),
+                   W2 = __shfl_up_sync(0xffffffffu, v.z, 1), W3 = __shfl_up_sync(0xffffffffu, v.w, 1);
+    const uint32_t W[8] = {W0, W1, W2, W3, v.x, v.y, v.z, v.w};
+    const uint32_t sft = 16u - r, m = sft >> 2;  // window (left 16 bytes, own 16 bytes) from byte sft
+    uint32_t B[6], V[5];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) B[j] = (m & 2u) ? W[j + 2] : W[j];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) V[k] = (m & 1u) ? B[k + 1] : B[k];
+    uint4 o;
+    if (A == 4) {
+        o = make_uint4(V[0], V[1], V[2], V[3]);
+    } else {
+        const uint32_t sel = (sft & 2u) ? 0x5432u : 0x3210u;
+        o = make_uint4(__byte_perm(V[0], V[1], sel), __byte_perm(V[1], V[2], sel), __byte_perm(V[2], V[3], sel),
+                       __byte_perm(V[3], V[4], sel));
+    }
+    if (ln >= 1 && ln <= 30) stg_cs_v4(reinterpret_cast<void *>(reinterpret_cast<uintptr_t>(q) - r), o);
+    if (ln == 0 || ln == 30) stg8<A>(q, v);
+}
+
 // the first nv (< 8) pixels of a lane that straddles the right edge (row-copy mode only)
 __device__ __forceinline__ void stg_partial(uint16_t *p, const uint4 v, const int nv) {
     const uint32_t q[4] = {v.x, v.y, v.z, v.w};
@@ -756,6 +794,11 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     // a lane may straddle the right edge; row-class TMA sums also mask lane 31 (max mode duplicates lane 30)
     constexpr bool kEdge = (AC != 16 && !FULL) || (kRT && !kMax);
     auto put = [&](const int k, const uint4 v) {
+        if (kRT && SSB_RT_SHIFT_STORES && FULL && acl<AC>() == 2) {
+            // every lane takes part in the shuffles (lane 31 lends nothing and stores nothing itself)
+            if (store) stg8_shift<acl<AC>()>(vrow + k * w, v, threadIdx.x & 31);
+            return;
+        }
         if (!(store && (FULL ? (!kRT || col_ok) : (k < rows_ok && col_ok)))) return;
         if (kEdge && nv < 8) stg_partial(vrow + k * w, v, nv);
         else if (kRT && SSB_RT_DYN_STORES && acl<AC>() == 8) stg8_any(vrow + k * w, v);
