@@ -532,7 +532,8 @@ __device__ __forceinline__ uint4 lds8(uint32_t a) {
 // for five / four 4-byte loads with the 4-way bank conflicts of a 16-byte lane stride), then a shift by a
 // whole word (a & 4) and, for 2-byte alignment, a half word (a & 2) -- both warp-uniform (the row's)
 // (projection-only kernels: W = 2046 / 2047 XY only 1.143 / 1.377 -> 1.095 / 1.323 ms, 3 MIPs 1.525 / 1.677
-// -> 1.486 / 1.612; with a volume they were 1-2.5 % slower, so volume kernels keep the 4-byte loads)
+// -> 1.486 / 1.612; volume kernels: at 4-byte rows 1 % slower, so they keep the 4-byte loads there; at 2-byte
+// rows, with the whole-sector stores below, 2.749 -> 2.686 ms, nearest 2.290 -> 2.188)
 #ifndef SSB_RT_W64_LOADS
 #define SSB_RT_W64_LOADS 2  // A/B knob: 0 off, 1 for 2-byte aligned taps, 2 also for 4-byte aligned taps
 #endif
@@ -550,7 +551,7 @@ __device__ __forceinline__ uint4 lds8_w64(uint32_t a) {
 
 template <int AC, bool W64 = false>
 __device__ __forceinline__ uint4 ldtap(uint32_t a) {
-    if (W64 && rt_mode<AC>() &&
+    if ((W64 || acl<AC>() == 2) && rt_mode<AC>() &&
         ((acl<AC>() == 2 && SSB_RT_W64_LOADS >= 1) || (acl<AC>() == 4 && SSB_RT_W64_LOADS >= 2)))
         return lds8_w64<acl<AC>()>(a);
     return lds8<smem_ac<AC>()>(a);
