@@ -171,6 +171,7 @@ struct Params {
     int32_t batch;
     int64_t vol_bstride, xy_bstride, xz_bstride, yz_bstride;
     int32_t rt_P, rt_B;  // row-class TMA: classes and box rows per class
+    int32_t rt_B31;      // row-class TMA: rows per class in the lane-31 blocks
     uint32_t rt_d0;      // row-class TMA: byte offset (mod 16) of frame row 0 (delta_c = (d0 + c*rs2) & 15)
 };
 
@@ -207,12 +208,20 @@ __host__ __device__ constexpr bool rt_mode() {
 // alignment (bytes) of the frame-row taps in shared memory and of the volume rows
 template <int AC>
 __host__ __device__ constexpr int acl() {
-    return AC > 16 ? AC - 32 : AC;
+    return AC > 16 ? AC & 31 : AC;
+}
+// Row-class TMA tiles are 248 columns wide (lane 31 idles: in max mode it duplicates lane 30, in sum mode its
+// voxels are masked) -- except projection-only launches with 8-byte rows (two classes, AC = 104 = 64 + 40):
+// there lane 31 reads its pixels from a small per-class box, so tiles keep 256 columns (W = 2044 XY only
+// 1.005 -> 0.955 ms, 3 MIPs 1.356 -> 1.300; with a volume, or 4 / 8 classes, it measured slower)
+template <int AC>
+__host__ __device__ constexpr bool lane31_boxes() {
+    return AC > 64;
 }
 // columns per tile
 template <int AC>
 __host__ __device__ constexpr int tile_w() {
-    return rt_mode<AC>() ? kTX - 8 : kTX;
+    return AC > 16 && !lane31_boxes<AC>() ? kTX - 8 : kTX;
 }
 template <int AC>
 __host__ __device__ constexpr int row_pitch() {
@@ -234,15 +243,29 @@ __host__ __device__ constexpr int box_rows_alloc() {
     return rt_mode<AC>() ? (16 / acl<AC>()) * rt_class_rows(Cfg<ROWS, SIDE>::kTU + 2, 16 / acl<AC>())
                          : Cfg<ROWS, SIDE>::kBoxRows;
 }
-// ring depth: the 4- / 8-class boxes take more rows per stage than one box
+// ring depth: the 4- / 8-class boxes take more rows per stage than one box, and the lane-31 blocks and
+// tables of the row-class mode leave no room for a fifth stage next to the XZ staging
 template <int ROWS, bool SIDE, int AC>
 __host__ __device__ constexpr int stage_count() {
     return rt_mode<AC>() && acl<AC>() < 8 ? Cfg<ROWS, SIDE>::kStages - 1 : Cfg<ROWS, SIDE>::kStages;
 }
 
+// row-class TMA: lane-31 block rows per stage (classes of B rows rounded up to 4: 128-byte aligned boxes)
+template <int ROWS, bool SIDE, int AC>
+__host__ __device__ constexpr int l31_rows_alloc() {
+    return lane31_boxes<AC>() ? (16 / acl<AC>()) * ((rt_class_rows(Cfg<ROWS, SIDE>::kTU + 2, 16 / acl<AC>()) + 3) / 4 * 4)
+                              : 1;
+}
+// max-mode slices per XZ hand-off: the lane-31 blocks of the 8-byte row-class mode take the room of a third
+// slice of XZ staging (a fifth ring stage is worth more)
+template <int ROWS, bool SIDE, int AC>
+__host__ __device__ constexpr int xz_batch() {
+    return lane31_boxes<AC>() && Cfg<ROWS, SIDE>::kXzBatch > 2 ? 2 : Cfg<ROWS, SIDE>::kXzBatch;
+}
+
 // tensor maps of one launch: [0] the frame box (TMA mode) or the row classes (row-class TMA mode)
 struct alignas(64) TmapSet {
-    CUtensorMap m[8];
+    CUtensorMap m[16];  // row-class TMA: [c] class c's 256-column boxes, [8 + c] its lane-31 boxes
 };
 
 template <int ROWS, int AC = 16, bool SIDE = true>
@@ -253,6 +276,10 @@ struct Smem {
     uint16_t zero_row[kTX + 8];
     // row-class TMA, regular stages: shared address of tap rows j0 + i of the stage (no lane offset)
     alignas(16) uint32_t taddr[rt_mode<AC>() ? kStages : 1][rt_mode<AC>() ? C::kTU + 4 : 4];
+    // row-class TMA: lane 31's pixels come from a 16-pixel box per class at map column x0 + 248 (lane 31's
+    // 8 pixels sit delta_c bytes into each 32-byte row), and its regular-stage tap addresses from taddr31
+    alignas(128) uint16_t l31[rt_mode<AC>() ? kStages : 1][rt_mode<AC>() ? l31_rows_alloc<ROWS, SIDE, AC>() : 1][16];
+    alignas(16) uint32_t taddr31[lane31_boxes<AC>() ? kStages : 1][lane31_boxes<AC>() ? C::kTU + 4 : 4];
     RowP rows[kStages][C::kTU];
     uint32_t hdr[kStages];  // bit 16: slice touches the tile; bits 0..14: warps with live rows;
                                // bits 17..31: warps whose rows chain their taps; bit 15: regular
@@ -260,7 +287,8 @@ struct Smem {
     StageP sp[kStages];
     CopyRec cp[kStages];     // consumer-copy mode: what to copy into each stage
     uint64_t geo[kStages];   // consumer-copy mode: cp[] of the stage's current use is published
-    alignas(16) uint32_t xz[C::kXzWords];
+    alignas(16) uint32_t xz[lane31_boxes<AC>() && C::kXzWords > 2 * kConsumerWarps * kTX ? 2 * kConsumerWarps * kTX
+                                                                                         : C::kXzWords];
     uint64_t full[kStages];
     uint64_t empty[kStages];
     uint64_t qfull[kQueue];
@@ -600,8 +628,9 @@ __device__ __forceinline__ void stg8_any(uint16_t *p, const uint4 v) {
 }
 
 // Row-class TMA volume rows that are 2- or 4-byte aligned: lane l's 16 bytes start r = (address & 15) past a
-// 16-byte boundary.  Lanes 1..30 store the aligned 16 bytes [q - r, q - r + 16) -- the left neighbour's last
-// r bytes and their own first 16 - r -- as one 16-byte store; lanes 0 and 30 also store their own 16 bytes
+// 16-byte boundary (248-column tiles: lanes 0..30).  Lanes 1..30 store the aligned 16 bytes [q - r, q - r + 16)
+// -- the left neighbour's last r bytes and their own first 16 - r -- as one 16-byte store; lanes 0 and 30 also
+// store their own 16 bytes
 // with narrow stores (covering the segment's unaligned head and tail; the overlap rewrites equal bytes).
 // Narrow 2- / 4-byte stores at a 16-byte lane stride write every sector in 4-8 pieces; this writes whole
 // sectors.  r is the same for every lane (lanes are 16 bytes apart), so the branch is uniform.
@@ -696,7 +725,15 @@ __device__ __forceinline__ void set_bracket(RowP &o, double w) {
 struct RtGeo {
     int64_t jb;
     uint32_t lp, B;  // log2(P), rows per class box
+    uint32_t B31;    // rows per class in the lane-31 blocks (B rounded up to 4: 128-byte aligned boxes)
+    uint32_t l31;    // shared address of the stage's lane-31 blocks
 };
+// lane 31's 8 pixels of frame row j: its class's lane-31 block, 32-byte rows, the row's byte offset
+__device__ __forceinline__ uint32_t row_addr31(int64_t j, uint32_t d0, uint32_t rs2, const RtGeo &g) {
+    const uint32_t q = (uint32_t)(j - g.jb);
+    const uint32_t c = q & ((1u << g.lp) - 1u), r = q >> g.lp;
+    return g.l31 + (c * g.B31 + r) * 32u + ((d0 + rs2 * (uint32_t)j) & 15u);
+}
 template <int AC>
 __device__ __forceinline__ uint32_t row_addr(int64_t j, int64_t box_r0, uint32_t box_addr, uint32_t d0, uint32_t rs2,
                                              const RtGeo &g) {
@@ -717,6 +754,8 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     o.off_a = o.off_b = zero_addr;
     o.kind = 3;
     o.pad = 0;
+    // row-class TMA (canvas formula: `kind` unused): kind / pad carry lane 31's tap addresses
+    if (lane31_boxes<AC>()) o.kind = o.pad = (int32_t)(zero_addr + 496u);
     if (FORMULA == SSB_FORMULA_NPINTERP) o.c0 = 0.0;  // t = 0: copy of tap a (the zero row)
     if (F64) {
         o.n0 = -(o.c0 * kTwo52);
@@ -731,10 +770,14 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     if (rp.j0 < box_r0 || rp.j1 < box_r0 || rp.j0 - box_r0 >= box_rows || rp.j1 - box_r0 >= box_rows) __trap();
     o.off_a = row_addr<AC>(rp.j0, box_r0, box_addr, d0, rs2, g);
     o.off_b = row_addr<AC>(rp.j1, box_r0, box_addr, d0, rs2, g);
+    if (lane31_boxes<AC>()) {
+        o.kind = (int32_t)row_addr31(rp.j0, d0, rs2, g);
+        o.pad = (int32_t)row_addr31(rp.j1, d0, rs2, g);
+    }
     if (rp.kind >= 2) {
         o.c0 = rp.c0;
         o.c1 = rp.c1;
-        o.kind = rp.kind;
+        if (!lane31_boxes<AC>()) o.kind = rp.kind;
         // weight of a + w*(b - a): canvas f; np.interp t (dx == 1) or t/dx
         if (F64) {
             o.n0 = -(rp.c0 * kTwo52);  // exact: power-of-two scaling
@@ -745,6 +788,7 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
     } else if (FORMULA == SSB_FORMULA_CANVAS) {
         // copy (only reachable for h == 1 paths): w0 = 1, f = 0
         o.off_b = o.off_a;
+        o.pad = o.kind;
     }
     return true;
 }
@@ -762,7 +806,8 @@ __device__ __forceinline__ bool make_row(RowP &o, int64_t u, bool in_window, int
 template <int INTERP, int FORMULA, bool kMax, bool FULL, int ROWS, bool SIDE, bool CHAIN, int AC, bool REG,
           bool NOVOL>
 __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_off, const uint32_t tap_base,
-                                          const uint32_t *tad, const StageP &sp, const int64_t u0,
+                                          const uint32_t *tad, const uint32_t *tad31, const StageP &sp,
+                                          const int64_t u0,
                                           uint16_t *vrow, const int64_t w, const int rows_ok, const bool col_ok,
                                           const int nv, uint4 (&acc_max)[ROWS],
                                           uint32_t (&acc_sum)[kMax ? 1 : ROWS][8],
@@ -778,29 +823,36 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
     constexpr bool chain = (CHAIN || REG) && INTERP == SSB_INTERP_LINEAR;
     constexpr uint32_t kPitch = 2u * row_pitch<AC>();
     constexpr bool kRT = rt_mode<AC>();
-    // row-class TMA, regular stage: the rows' tap addresses from the stage's table (consecutive rows
+    // row-class TMA: lane 31 reads its taps from the stage's lane-31 blocks (rows of 32 bytes)
+    constexpr bool kL31 = lane31_boxes<AC>();
+    constexpr bool kT248 = kRT && !kL31;  // 248-column tiles: lane 31 outside the tile
+    const bool l31 = kL31 && (threadIdx.x & 31) == 31;
+    // row-class TMA, regular stage: the rows' tap addresses from the stage's tables (consecutive rows
     // alternate between class boxes)
     uint32_t ta[ROWS + 1];
     if (kRT && REG) {
 #pragma unroll
-        for (int k = 0; k <= ROWS; ++k) ta[k] = tad[k] + lane_off;
+        for (int k = 0; k <= ROWS; ++k) ta[k] = kL31 && l31 ? tad31[k] : tad[k] + lane_off;
     }
-    // tap addresses of row k (lane offset included)
+    // tap addresses of row k (lane offset included; row-class TMA lane 31: the row table's kind / pad)
     auto tap_a = [&](const int k) {
-        return REG ? (kRT ? ta[k] : tap_base + (uint32_t)k * kPitch) : rg[k].off_a + lane_off;
+        return REG ? (kRT ? ta[k] : tap_base + (uint32_t)k * kPitch)
+                   : (l31 ? (uint32_t)rg[k].kind : rg[k].off_a + lane_off);
     };
     auto tap_b = [&](const int k) {
-        return REG ? (kRT ? ta[k + 1] : tap_base + (uint32_t)(k + 1) * kPitch) : rg[k].off_b + lane_off;
+        return REG ? (kRT ? ta[k + 1] : tap_base + (uint32_t)(k + 1) * kPitch)
+                   : (l31 ? (uint32_t)rg[k].pad : rg[k].off_b + lane_off);
     };
-    // a lane may straddle the right edge; row-class TMA sums also mask lane 31 (max mode duplicates lane 30)
-    constexpr bool kEdge = (AC != 16 && !FULL) || (kRT && !kMax);
+    // a lane may straddle the right edge; 248-column tiles in sum mode also mask lane 31 (max mode
+    // duplicates lane 30)
+    constexpr bool kEdge = (AC != 16 && !FULL) || (kT248 && !kMax);
     auto put = [&](const int k, const uint4 v) {
         if (kRT && SSB_RT_SHIFT_STORES && FULL && acl<AC>() == 2) {
             // every lane takes part in the shuffles (lane 31 lends nothing and stores nothing itself)
             if (store) stg8_shift<acl<AC>()>(vrow + k * w, v, threadIdx.x & 31);
             return;
         }
-        if (!(store && (FULL ? (!kRT || col_ok) : (k < rows_ok && col_ok)))) return;
+        if (!(store && (FULL ? (!kT248 || col_ok) : (k < rows_ok && col_ok)))) return;
         if (kEdge && nv < 8) stg_partial(vrow + k * w, v, nv);
         else if (kRT && SSB_RT_DYN_STORES && acl<AC>() == 8) stg8_any(vrow + k * w, v);
         else stg8<acl<AC>()>(vrow + k * w, v);
@@ -990,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // consumer-copy mode: stages copied ahead of the one processed; copying stage k + D needs every warp
     // done with stage k + D - kStages, so D < kStages - 1 leaves the warps room to drift apart
     constexpr int kLookahead = kStages - SSB_LOOKAHEAD_GAP > 0 ? kStages - SSB_LOOKAHEAD_GAP : 1;
-    constexpr int kXzBatch = kMax ? C::kXzBatch : 1;
+    constexpr int kXzBatch = kMax ? xz_batch<ROWS, SIDE, AC>() : 1;
     static_assert(kXzBatch * (kTX / 2) <= kConsumerThreads, "one consumer thread per (slice, column pair)");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<ROWS, AC, SIDE> &sm = *reinterpret_cast<Smem<ROWS, AC, SIDE> *>(smem_raw);
@@ -1015,7 +1067,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == kConsumerWarps) {
         // ===================== producer warp =====================
-        if (lane < (kRT ? p.rt_P : 1)) prefetch_tmap(&maps.m[lane]);
+        if (kRT ? (lane < p.rt_P || (lane31_boxes<AC>() && lane >= 8 && lane < 8 + p.rt_P)) : lane == 0)
+            prefetch_tmap(&maps.m[lane]);
         // L2 policy of the frame loads: evict-normal in max mode (measured 2-3 % faster isolated:
         // halo rows shared by vertically adjacent tiles survive), evict-first in sum mode (whose u32
         // REDs into the caller's outputs want the L2 space; evict-normal was 2 % slower there)
@@ -1059,10 +1112,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // while it is in flight (full completes on the bytes + all 32 lane arrivals)
                 constexpr int kBoxRowsUsed = C::template box_rows<INTERP, FORMULA>();
                 // row-class TMA: the class boxes start at frame row jb (the multiple of P at or below box_r0)
-                RtGeo rg{0, 0, 0};
+                RtGeo rg{0, 0, 0, 0, 0};
                 if (kRT) {
                     rg.lp = (uint32_t)(__ffs(p.rt_P) - 1);
                     rg.B = (uint32_t)p.rt_B;
+                    rg.B31 = (uint32_t)p.rt_B31;
+                    rg.l31 = smem_addr(&sm.l31[stage][0][0]);
                     rg.jb = (box_r0 >> rg.lp) << rg.lp;  // floor (arithmetic shift)
                 }
                 if (lane == 0) {
@@ -1073,10 +1128,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     frame0 + (int32_t)s, policy);
                     }
                     if (hit && kRT) {
-                        mbar_expect_tx(&sm.full[stage], (uint32_t)(p.rt_P * p.rt_B) * kRowBytes);
-                        for (int c = 0; c < p.rt_P; ++c)
+                        // per class: the 256-column box (and lane 31's 16-column box at map column x0 + 248)
+                        mbar_expect_tx(&sm.full[stage],
+                                       (uint32_t)(p.rt_P * p.rt_B) * (kRowBytes + (lane31_boxes<AC>() ? 32u : 0u)));
+                        for (int c = 0; c < p.rt_P; ++c) {
                             tma_load_3d(&sm.box[stage][c * p.rt_B][0], &maps.m[c], &sm.full[stage], xt * kTW,
                                         (int32_t)(rg.jb >> rg.lp), (int32_t)s, policy);
+                            if (lane31_boxes<AC>())
+                                tma_load_3d(&sm.l31[stage][c * p.rt_B31][0], &maps.m[8 + c], &sm.full[stage],
+                                            xt * kTW + kTW - 8, (int32_t)(rg.jb >> rg.lp), (int32_t)s, policy);
+                        }
                     }
                 }
                 __syncwarp();
@@ -1175,7 +1236,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < (kTU + 1 + 31) / 32; ++j) {
                             const int i = lane + 32 * j;
-                            if (i <= kTU) sm.taddr[stage][i] = row_addr<AC>(spv.j0 + i, box_r0, box_addr, d0, rs2, rg);
+                            if (i <= kTU) {
+                                const uint32_t a = row_addr<AC>(spv.j0 + i, box_r0, box_addr, d0, rs2, rg);
+                                sm.taddr[stage][i] = a;
+                                if (lane31_boxes<AC>()) sm.taddr31[stage][i] = row_addr31(spv.j0 + i, d0, rs2, rg);
+                            }
                         }
                     }
                     if (regular && lane == 0) {
@@ -1243,8 +1308,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== consumer warps =====================
     uint32_t stage = 0, sphase = 0, q = 0, qphase = 0, xz_batch = 0;
     const size_t plane = (size_t)p.u_count * p.w;
-    // row-class TMA, max mode: lane 31 (outside the 248-column tile) duplicates lane 30's columns
-    const uint32_t lane_off = (kRT && kMax ? min(lane, 30) : lane) * 16;
+    constexpr bool kT248 = kRT && !lane31_boxes<AC>();  // 248-column tiles: lane 31 outside the tile
+    // 248-column tiles, max mode: lane 31 duplicates lane 30's columns
+    const uint32_t lane_off = (kT248 && kMax ? min(lane, 30) : lane) * 16;
     // consumer-copy mode: copy this warp's share (rows r with r % 15 == warp) of stage g's box rows,
     // then arrive on its `full` barrier when the copies have landed
     uint32_t g_next = 0;  // next stage (in the global stage sequence) to copy for
@@ -1293,9 +1359,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int64_t s_begin, s_end;
         decode<kTU>(item, p, b, ut, xt, s_begin, s_end);
         const int64_t x = (int64_t)xt * kTW + lane * 8;
-        const bool col_ok = x < p.w && (!kRT || lane < 31);
-        // this lane's pixels inside (row-class TMA: lane 31 has none)
-        const int nv = (kRT && lane == 31) ? 0 : (int)max((int64_t)0, min((int64_t)8, p.w - x));
+        const bool col_ok = x < p.w && (!kT248 || lane < 31);
+        // this lane's pixels inside (248-column tiles: lane 31 has none)
+        const int nv = (kT248 && lane == 31) ? 0 : (int)max((int64_t)0, min((int64_t)8, p.w - x));
         const int64_t r0 = (int64_t)ut * kTU + warp * ROWS;  // window row of k = 0
         const int64_t rows_left = p.u_count - r0;
         const int rows_ok = rows_left <= 0 ? 0 : (rows_left >= ROWS ? ROWS : (int)rows_left);
@@ -1304,7 +1370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              : nullptr;
         // warp-uniform fast path: every lane's 8 columns and all rows inside the output
         const bool fast =
-            __all_sync(0xffffffffu, AC == 16 ? col_ok : (nv == 8 || (kRT && lane == 31))) && rows_ok == ROWS;
+            __all_sync(0xffffffffu, AC == 16 ? col_ok : (nv == 8 || (kT248 && lane == 31))) && rows_ok == ROWS;
         // SIDE == false kernels run only without XZ / YZ outputs: their blocks compile away
         uint32_t *yzp = (SIDE && p.yz != nullptr) ? p.yz + b * p.yz_bstride + (size_t)s_begin * p.u_count + r0 + lane
                                                   : nullptr;
@@ -1341,7 +1407,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool chained = (hdr >> (17 + warp)) & 1u;
                 const int64_t u0 = p.u_begin + r0;  // canvas row of this warp's row 0
 #define SSB_ROWS_PASS(F, CH, RG)                                                                             \
-    rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG, !VOL>(rg, lane_off, tap_base, tad, spv, u0, vrow, p.w, rows_ok, \
+    rows_pass<INTERP, FORMULA, kMax, F, ROWS, SIDE, CH, AC, RG, !VOL>(rg, lane_off, tap_base, tad, tad31, spv, \
+                                                                     u0, vrow, p.w, rows_ok, \
                                                             col_ok, nv, acc_max, acc_sum, xz_max, xz_sum, yzv)
                 if ((AC == 16 || consumer_copy<AC>() || kRT) && FORMULA == SSB_FORMULA_CANVAS && !kF64 &&
                     ((hdr >> 15) & 1u)) {
@@ -1349,6 +1416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     StageP spv = sm.sp[stage];
                     spv.j0 += warp * ROWS;  // frame row of tap a of this warp's row 0
                     const uint32_t *tad = kRT ? &sm.taddr[stage][warp * ROWS] : nullptr;
+                    const uint32_t *tad31 = lane31_boxes<AC>() ? &sm.taddr31[stage][warp * ROWS] : nullptr;
                     const uint32_t tap_base = smem_addr(&sm.box[stage][0][0]) +
                                               (uint32_t)(spv.a0 + warp * ROWS) * (2u * row_pitch<AC>()) + lane_off;
                     if (fast) SSB_ROWS_PASS(true, true, true);
@@ -1356,7 +1424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                     const StageP spv{};
                     const uint32_t tap_base = 0;
-                    const uint32_t *tad = nullptr;
+                    const uint32_t *tad = nullptr, *tad31 = nullptr;
                     // four specialisations so the row loop has no per-row branches
                     if (fast) {
                         if (chained) SSB_ROWS_PASS(true, true, false);
@@ -1545,6 +1613,9 @@ int launch_kernel(const TmapSet &map, const Params &prm, int grid, cudaStream_t 
 // projection-only calls (no volume) of the TMA mode get the instantiation without store code
 template <int INTERP, int FORMULA, int REDUCE, int ROWS, bool SIDE, int AC>
 int launch_one(const TmapSet &map, const Params &prm, int grid, cudaStream_t st) {
+    if constexpr (lane31_boxes<AC>()) {  // chosen for projection-only launches only
+        return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, false>(map, prm, grid, st);
+    }
     if ((AC == 16 || consumer_copy<AC>() || rt_mode<AC>()) && prm.vol == nullptr)
         return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, false>(map, prm, grid, st);
     return launch_kernel<INTERP, FORMULA, REDUCE, ROWS, SIDE, AC, true>(map, prm, grid, st);
@@ -1579,6 +1650,7 @@ int launch_ac(int ac, bool mx, bool tall, bool side, const TmapSet &map, const P
         if (ac == 40) return launch_variant<INTERP, FORMULA, 40>(mx, false, side, map, prm, grid, st);
         if (ac == 36) return launch_variant<INTERP, FORMULA, 36>(mx, false, side, map, prm, grid, st);
         if (ac == 34) return launch_variant<INTERP, FORMULA, 34>(mx, false, side, map, prm, grid, st);
+        if (ac == 104) return launch_variant<INTERP, FORMULA, 104>(mx, false, side, map, prm, grid, st);
     }
     return fail(SSB_ERR_PARAM, "no persistent kernel for access class %d", ac);
 }
@@ -1663,7 +1735,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     }
     // Rows that are not 16-byte aligned (canvas lerp, one stack, frames 16 bytes apart): one tensor map per
     // row class (see rt_mode) instead of the row-copy modes.  P = 16 / gcd(2 * row_stride, 16) classes.
-    int32_t rt_P = 0, rt_B = 0;
+    int32_t rt_P = 0, rt_B = 0, rt_B31 = 0;
     uint32_t rt_d0 = 0;
     {
         const int64_t rs = row_stride_of(d), fs = frame_stride_of(d);
@@ -1681,15 +1753,22 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
                                           (cuuint64_t)((d.height - c + P - 1) / P), (cuuint64_t)d.n};
                 const cuuint64_t cs[2] = {(cuuint64_t)(2 * P * rs), (cuuint64_t)(2 * fs)};
                 const cuuint32_t cb[3] = {(cuuint32_t)kTX, (cuuint32_t)B, 1};
+                const cuuint32_t cb31[3] = {16, (cuuint32_t)B, 1};  // lane 31's box (16 columns)
                 ok = encode_fn()(&maps.m[c], CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, reinterpret_cast<void *>(a - dlt), cd, cs,
                                  cb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, SSB_L2_PROMO,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+                     (ac != 8 ||
+                      encode_fn()(&maps.m[8 + c], CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, reinterpret_cast<void *>(a - dlt), cd,
+                                 cs, cb31, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 SSB_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS);
             }
             if (ok) {
                 rt_P = P;
                 rt_B = B;
+                rt_B31 = (B + 3) / 4 * 4;
                 rt_d0 = (uint32_t)(r0 & 15u);
                 ac += 32;
+                if (ac == 40 && vol == nullptr) ac += 64;  // projection-only, 8-byte rows: lane-31 boxes
             }
         }
     }
@@ -1698,7 +1777,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     // dynamic scheduler's tail short (projections reduce in L2, so chunking costs no partial planes)
     const int sms = num_sms();
     const int64_t UT = std::max<int64_t>(1, (d.u_count + kTU - 1) / kTU);
-    const int64_t tw = ac > 16 ? kTX - 8 : kTX;  // tile width (row-class TMA: 248)
+    const int64_t tw = ac > 16 && ac < 64 ? kTX - 8 : kTX;  // tile width (row-class TMA: 248 unless lane-31 boxes)
     const int64_t XT = std::max<int64_t>(1, (d.width + tw - 1) / tw);
     const int64_t tiles = UT * XT * batch;  // tiles of every stack of the batch
     // phase 1: ~SSB_ITEMS_PER_CTA big items per CTA over the first SSB_BIG_PERCENT % of the
@@ -1802,6 +1881,7 @@ int launch_deskew_tma(const ssb_deskew_desc &d, const uint16_t *raw, uint16_t *v
     prm.yz_bstride = (int64_t)s_yz;
     prm.rt_P = rt_P;
     prm.rt_B = rt_B;
+    prm.rt_B31 = rt_B31;
     prm.rt_d0 = rt_d0;
     const int grid = (int)std::min<int64_t>(items, sms);
 
