@@ -42,20 +42,41 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel (the persistent kernel's instantiations are split
+    over several translation units), then link the shared library."""
     if not force and not needs_build():
         return OUT
+    from concurrent.futures import ThreadPoolExecutor
+
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    tmp = OUT + ".tmp"
+    objdir = os.path.join(os.path.dirname(OUT), "obj")
+    os.makedirs(objdir, exist_ok=True)
     extra = os.environ.get("SSB_NVCC_EXTRA", "").split()  # A/B variants, e.g. -DSSB_MAGIC_CVT
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-o", tmp, *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [nvcc(), *compile_flags, *extra, "-I", os.path.join(REPO, "include"), "-c", "-o", obj, src]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as pool:
+        results = list(pool.map(compile_one, srcs))
+    log = []
+    for obj, res in results:
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
+        log.append(res.stderr)
+    tmp = OUT + ".tmp"
+    res = subprocess.run([nvcc(), "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *(o for o, _ in results)],
+                         capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
+        raise RuntimeError(f"nvcc link failed:\n{res.stdout}\n{res.stderr}")
     if verbose:
-        print(res.stderr)
+        print("".join(log))
     os.replace(tmp, OUT)
     with open(os.path.join(os.path.dirname(OUT), "ptxas.log"), "w") as f:
-        f.write(res.stderr)
+        f.write("".join(log))
     return OUT
 
 

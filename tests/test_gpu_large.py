@@ -162,7 +162,7 @@ def test_config5_full_scan_sum_matches_oracle():
     slice indices, per-slab canvas row windows) merged on the device, are both compared with the C
     oracle run chunk by chunk (512 frames, global indices) and accumulated in uint64 on the host.
     Full 16-bit range, so the fp32 bracket's fallback and the per-tile slice-range clipping
-    (ssb_deskew_tma.cu tile_slices) are exercised where a long scan stresses them most.
+    (ssb_tma_kernel.cuh tile_slices) are exercised where a long scan stresses them most.
     """
     from paper_2211_00645_b200 import dist as D
     from paper_2211_00645_b200.deskew import canvas_rows_for
