@@ -932,7 +932,6 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
             if (chain64) {
                 double cur[8];
                 to_biased8(ldtap<AC, NOVOL>(tap_b(k)), cur);
-                uint32_t r[8];
                 lerp_biased8_raw(prevd, cur, c0, c1, rg[k].n0, rg[k].n1, bits);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) prevd[c] = cur[c];
