@@ -258,11 +258,21 @@ __host__ __device__ constexpr int l31_rows_alloc() {
     return lane31_boxes<AC>() ? (16 / acl<AC>()) * ((rt_class_rows(Cfg<ROWS, SIDE>::kTU + 2, 16 / acl<AC>()) + 3) / 4 * 4)
                               : 1;
 }
-// max-mode slices per XZ hand-off: the lane-31 blocks of the 8-byte row-class mode take the room of a third
-// slice of XZ staging (a fifth ring stage is worth more)
+// Staged YZ (TMA mode, 4-row tiles with side projections, max mode): each lane's per-row u16x2 candidate
+// words go to shared memory with the XZ partials, and threads of the XZ hand-off fold each row pair's 32
+// words after the batch barrier -- no per-row split + `redux` on the consumers (3 MIPs 1.158 -> 1.126 ms,
+// XY+XZ 1.094 -> 1.088; a YZ-only view now takes the batch barrier too: XY+YZ 1.060 -> 1.113).
+template <int ROWS, bool SIDE, int AC>
+__host__ __device__ constexpr bool staged_yz() {
+    return AC == 16 && SIDE && ROWS == 4;
+}
+// max-mode slices per XZ hand-off: the lane-31 blocks of the 8-byte row-class mode, and the YZ staging,
+// take the room of a third slice of XZ staging
 template <int ROWS, bool SIDE, int AC>
 __host__ __device__ constexpr int xz_batch() {
-    return lane31_boxes<AC>() && Cfg<ROWS, SIDE>::kXzBatch > 2 ? 2 : Cfg<ROWS, SIDE>::kXzBatch;
+    return (lane31_boxes<AC>() || staged_yz<ROWS, SIDE, AC>()) && Cfg<ROWS, SIDE>::kXzBatch > 2
+               ? 2
+               : Cfg<ROWS, SIDE>::kXzBatch;
 }
 
 // tensor maps of one launch: [0] the frame box (TMA mode) or the row classes (row-class TMA mode)
@@ -289,8 +299,12 @@ struct Smem {
     StageP sp[kStages];
     CopyRec cp[kStages];     // consumer-copy mode: what to copy into each stage
     uint64_t geo[kStages];   // consumer-copy mode: cp[] of the stage's current use is published
-    alignas(16) uint32_t xz[lane31_boxes<AC>() && C::kXzWords > 2 * kConsumerWarps * kTX ? 2 * kConsumerWarps * kTX
-                                                                                         : C::kXzWords];
+    alignas(16) uint32_t xz[(lane31_boxes<AC>() || staged_yz<ROWS, SIDE, AC>()) && C::kXzWords > 2 * kConsumerWarps * kTX
+                                ? 2 * kConsumerWarps * kTX
+                                : C::kXzWords];
+    // staged YZ: [buffer][slice of the batch][row pair][32 lane words, swizzled by (row pair & 7) << 2]
+    alignas(16) uint32_t yzs[staged_yz<ROWS, SIDE, AC>() ? 2 : 1][staged_yz<ROWS, SIDE, AC>() ? 2 : 1]
+                            [staged_yz<ROWS, SIDE, AC>() ? C::kTU / 2 : 1][32];
     uint64_t full[kStages];
     uint64_t empty[kStages];
     uint64_t qfull[kQueue];
@@ -698,6 +712,11 @@ __device__ __forceinline__ uint32_t hmax8(const uint4 v) {
     return max(m & 0xFFFFu, m >> 16);
 }
 
+// the same as a u16x2 word (both halves candidates)
+__device__ __forceinline__ uint32_t hmax8w(const uint4 v) {
+    return __vmaxu2(__vmaxu2(__vmaxu2(v.x, v.y), v.z), v.w);
+}
+
 __device__ __forceinline__ uint32_t redux_max(uint32_t v) {
     uint32_t r;
     asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
@@ -871,7 +890,8 @@ __device__ __forceinline__ void rows_pass(const RowP *rg, const uint32_t lane_of
                 } else if (!kFoldXz) {
                     xz_max = max_u16x8(xz_max, v);
                 }
-                yzv[k] = redux_max(hmax8(v));
+                // staged YZ: the lane's u16x2 candidate word (folded across lanes after the pass)
+                yzv[k] = staged_yz<ROWS, SIDE, AC>() ? hmax8w(v) : redux_max(hmax8(v));
             }
         } else {
             const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
@@ -1045,6 +1065,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kLookahead = kStages - SSB_LOOKAHEAD_GAP > 0 ? kStages - SSB_LOOKAHEAD_GAP : 1;
     constexpr int kXzBatch = kMax ? xz_batch<ROWS, SIDE, AC>() : 1;
     static_assert(kXzBatch * (kTX / 2) <= kConsumerThreads, "one consumer thread per (slice, column pair)");
+    static_assert(!(kMax && staged_yz<ROWS, SIDE, AC>()) ||
+                      (kXzBatch <= 2 && kXzBatch * (kTX / 2 + kTU / 2) <= kConsumerThreads),
+                  "staged YZ: one consumer thread per (slice, row pair) next to the XZ threads");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<ROWS, AC, SIDE> &sm = *reinterpret_cast<Smem<ROWS, AC, SIDE> *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1450,7 +1473,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++stage == kStages) { stage = 0; sphase ^= 1; }
             if (vrow != nullptr) vrow += plane;
 
-            if (yzp != nullptr) {
+            constexpr bool kYS = kMax && staged_yz<ROWS, SIDE, AC>();
+            if (!kYS && yzp != nullptr) {
 #if SSB_YZ_LIVE_ONLY
                 // dead passes have all-zero rows (neutral for max and sum): no RED, no lane select
                 if (live && lane < rows_ok) {
@@ -1472,12 +1496,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 yzp += p.u_count;
             }
 
-            if (has_xz) {
+            if (has_xz || (kYS && yzp != nullptr)) {
                 const int buf = xz_batch & 1;
-                if (kMax) {
+                if (kYS && yzp != nullptr) {
+                    // this warp's row pairs (4w, 4w+1) and (4w+2, 4w+3): u16x2 words (pair's first row low)
+                    const uint32_t t01 = __vmaxu2(__byte_perm(yzv[0], yzv[1], 0x5410), __byte_perm(yzv[0], yzv[1], 0x7632));
+                    const uint32_t t23 = __vmaxu2(__byte_perm(yzv[2], yzv[3], 0x5410), __byte_perm(yzv[2], yzv[3], 0x7632));
+                    const int rp0 = warp * 2, rp1 = rp0 + 1;
+                    sm.yzs[buf][g][rp0][lane ^ ((rp0 & 7) << 2)] = t01;
+                    sm.yzs[buf][g][rp1][lane ^ ((rp1 & 7) << 2)] = t23;
+                }
+                if (kMax && has_xz) {
                     uint32_t *dst = &sm.xz[((buf * kXzBatch + g) * kConsumerWarps + warp) * (kTX / 2) + lane * 4];
                     *reinterpret_cast<uint4 *>(dst) = xz_max;
-                } else {
+                } else if (!kMax) {
                     uint32_t *dst = &sm.xz[(buf * kConsumerWarps + warp) * kTX + lane * 8];
                     if (kBiased && live) {
 #pragma unroll
@@ -1489,7 +1521,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (g == kXzBatch - 1 || si + 1 == ns) {
                     named_bar_sync(1, kConsumerThreads);
                     const int64_t s0 = s_begin + si - g;  // first slice of this batch
-                    if (kMax) {
+                    if (kYS && yzp != nullptr && tid >= kXzBatch * (kTX / 2) &&
+                        tid < kXzBatch * (kTX / 2) + kXzBatch * (kTU / 2)) {
+                        // thread -> (slice of batch, row pair): max over the pair's 32 lane words, read in
+                        // the swizzled order (conflict-free across the reducing threads)
+                        const int t2 = tid - kXzBatch * (kTX / 2), gg = t2 / (kTU / 2), rp = t2 % (kTU / 2);
+                        if (gg <= g) {
+                            const uint32_t base = smem_addr(&sm.yzs[buf][gg][rp][0]);
+                            uint4 a = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) a = max_u16x8(a, lds128(base + 16u * (uint32_t)(q ^ (rp & 7))));
+                            const uint32_t m = __vmaxu2(__vmaxu2(a.x, a.y), __vmaxu2(a.z, a.w));
+                            const int64_t wr = (int64_t)ut * kTU + 2 * rp;  // window row of the pair's first row
+                            uint32_t *dst = p.yz + b * p.yz_bstride + (size_t)(s0 + gg) * p.u_count + wr;
+                            if ((m & 0xFFFFu) && wr < p.u_count) red_u32<true>(dst, m & 0xFFFFu);
+                            if ((m >> 16) && wr + 1 < p.u_count) red_u32<true>(dst + 1, m >> 16);
+                        }
+                    }
+                    if (kMax && has_xz) {
                         // thread -> (slice of batch, word of 2 columns)
                         const int gg = tid / (kTX / 2), c2 = tid % (kTX / 2);
                         const int64_t col = (int64_t)xt * kTW + 2 * c2;
@@ -1502,7 +1551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (red & 0xFFFFu) red_u32<true>(dst, red & 0xFFFFu);
                             if (red >> 16) red_u32<true>(dst + 1, red >> 16);
                         }
-                    } else if (tid < kTW) {
+                    } else if (!kMax && tid < kTW) {
                         const int64_t col = (int64_t)xt * kTW + tid;
                         if (col < p.w) {
                             uint32_t red = 0;
